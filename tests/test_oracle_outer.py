@@ -1,0 +1,253 @@
+"""Pins of the oracle's receive side and whole rounds (or_decode_mean,
+or_nesterov, or_merge, or_apply, or_round, or_toy_run) against:
+  * SPEC examples (golden/paper_examples.json): Nesterov -0.76 / 1.084,
+    merge (2,2)/(0,4) -> (1,3), on-grid exact mean, {x, -x} -> 0;
+  * the library routine torch.optim.SGD(nesterov=True) (operand-scaled
+    tolerance: torch's CPU kernels may contract into FMA; momentum bitwise);
+  * textbook reductions: FedAvg (lr=1, mu=0, alpha=0 -> parameter average,
+    P:13), M=1 identity, H=1 data-parallel averaging, and
+    Streaming with P=1, tau=0 == DiLoCo (Alg. 1);
+  * invariants: alpha=1 leaves theta unchanged while momentum advances
+    (P:137); momentum advances once per round regardless of M.
+On-grid data: A = k 2^-20, Delta in {0, +-2^-8 2^-j},
++-2^-8 present in every block, theta = A - Delta (exact)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def on_grid(rng, n, B):
+    A = (rng.integers(-(2 ** 21) + 1, 2 ** 21, n) * 2.0 ** -20).astype(np.float32)
+    mags = np.concatenate([[0.0], 2.0 ** -8 * 2.0 ** -np.arange(7)])
+    D = (rng.choice(mags, n) * rng.choice([-1.0, 1.0], n)).astype(np.float32)
+    blen = B if B else n
+    D[::blen] = 2.0 ** -8  # every block holds the max -> scale 2^-8
+    th = (A - D).astype(np.float32)
+    assert np.array_equal((A - th).astype(np.float32), D)
+    return A, D, th
+
+
+def bits(x):
+    return np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+
+
+def test_nesterov_spec_examples():
+    g = GOLD["nesterov"]
+    A = np.array([5.0], np.float32)
+    v = np.zeros(1, np.float32)
+    one = np.ones(1, np.float32)
+    oracle.nesterov(A, v, one, g["lr"], g["mu"])
+    assert v[0] == 1.0
+    assert abs((5.0 - A[0]) - g["first_update"]) <= 4 * np.spacing(np.float32(5.0))
+    A2 = A.copy()
+    oracle.nesterov(A2, v, one, g["lr"], g["mu"])
+    assert abs((A[0] - A2[0]) - g["second_update"]) <= 4 * np.spacing(np.float32(5.0))
+    # mu = 0 is plain SGD exactly
+    A3, v3 = np.array([1.25], np.float32), np.array([7.0], np.float32)
+    gg = np.array([0.375], np.float32)
+    oracle.nesterov(A3, v3, gg, 0.5, 0.0)
+    assert A3[0] == np.float32(1.25) - np.float32(0.5) * np.float32(0.375) and v3[0] == gg[0]
+
+
+def test_nesterov_vs_torch_sgd():
+    rng = np.random.default_rng(11)
+    n = 100000
+    A = rng.standard_normal(n).astype(np.float32)
+    v = (rng.standard_normal(n) * 0.1).astype(np.float32)
+    for step in range(3):
+        g = (rng.standard_normal(n) * 0.05).astype(np.float32)
+        p = torch.nn.Parameter(torch.from_numpy(A.copy()))
+        opt = torch.optim.SGD([p], lr=0.4, momentum=0.9, nesterov=True, dampening=0.0)
+        opt.state[p]["momentum_buffer"] = torch.from_numpy(v.copy())
+        p.grad = torch.from_numpy(g.copy())
+        opt.step()
+        oracle.nesterov(A, v, g, 0.4, 0.9)
+        assert np.array_equal(bits(opt.state[p]["momentum_buffer"].numpy()), bits(v))
+        ref = p.detach().numpy()
+        scale = np.maximum.reduce([np.abs(ref), 0.4 * np.abs(g), 0.4 * 0.9 * np.abs(v)])
+        assert np.all(np.abs(ref - A) <= 16 * 2.0 ** -24 * scale)
+        A = ref.copy()  # continue from the library's state
+
+
+def test_merge_spec_examples():
+    g = GOLD["merge"]
+    th = np.array(g["theta"], np.float32)
+    oracle.merge(th, np.array(g["tilde"], np.float32), g["alpha"])
+    assert th.tolist() == g["merged"]
+    th = np.array([1.5, -2.0], np.float32)
+    oracle.merge(th, np.array([9.0, 9.0], np.float32), 1.0)  # alpha = 1: no communication
+    assert th.tolist() == [1.5, -2.0]
+    oracle.merge(th, np.array([9.0, -3.0], np.float32), 0.0)  # alpha = 0: theta = tilde
+    assert th.tolist() == [9.0, -3.0]
+
+
+@pytest.mark.parametrize("M", [1, 2, 4, 8])
+def test_mean_exact_on_grid(M):
+    rng = np.random.default_rng(M)
+    n, B = 3000, 1024
+    A = np.zeros(n, np.float32)
+    Ds, slots = [], []
+    for m in range(M):
+        _, D, _ = on_grid(rng, n, B)
+        Ds.append(D)
+        pay, _ = oracle.quantize(np.zeros(n, np.float32), D, B)  # Delta = D - 0
+        slots.append(pay)
+    g = oracle.decode_mean(np.concatenate(slots), M, n, B)
+    assert np.array_equal(g.astype(np.float64), np.mean(np.stack(Ds).astype(np.float64), axis=0))
+    if M == 2:  # {x, -x} -> 0
+        p1, _ = oracle.quantize(np.zeros(n, np.float32), Ds[0], B)
+        p2, _ = oracle.quantize(np.zeros(n, np.float32), -Ds[0], B)
+        assert not oracle.decode_mean(np.concatenate([p1, p2]), 2, n, B).any()
+
+
+@pytest.mark.parametrize("M", [1, 2, 4, 8])
+def test_fedavg_reduction(M):
+    """lr = 1, mu = 0, alpha = 0: the anchor becomes the plain parameter
+    average (1/M) sum_m theta_m (FedAvg), bit-exact on grid."""
+    rng = np.random.default_rng(100 + M)
+    n, B = 4096 + 333, 1024
+    A, _, _ = on_grid(rng, n, B)
+    thetas = []
+    for m in range(M):
+        _, D, _ = on_grid(rng, n, B)
+        thetas.append((A - D).astype(np.float32))
+    merges = [t.copy() for t in thetas]
+    Aw, v = A.copy(), np.zeros(n, np.float32)
+    st, _ = oracle.round_(thetas, merges, Aw, v, B=B, lr=1.0, mu=0.0, alpha=0.0)
+    assert st == 0
+    avg = np.mean(np.stack(thetas).astype(np.float64), axis=0)
+    assert np.array_equal(Aw.astype(np.float64), avg)
+    for mth in merges:
+        assert np.array_equal(bits(mth), bits(Aw))
+
+
+def test_m1_identity():
+    rng = np.random.default_rng(5)
+    n = 2048 + 17
+    A, D, th = on_grid(rng, n, 1024)
+    drift = (th - np.float32(2.0 ** -10)).astype(np.float32)
+    merged = [drift.copy()]
+    Aw, v = A.copy(), np.zeros(n, np.float32)
+    st, _ = oracle.round_([th], merged, Aw, v, B=1024, lr=1.0, mu=0.0, alpha=0.0)
+    assert st == 0 and np.array_equal(bits(merged[0]), bits(th)) and np.array_equal(bits(Aw), bits(th))
+
+
+def test_h1_data_parallel_averaging():
+    """P = 1, H = 1, tau = 0, lr = 1, mu = 0, alpha = 0: every step equals
+    data-parallel averaging of the replicas' updates: the
+    reference averages the per-replica updates (what an AVG all-reduce of
+    the gradients computes) and applies them to one shared copy."""
+    rng = np.random.default_rng(9)
+    n, M, B = 1500, 4, 1024
+    A0, _, _ = on_grid(rng, n, B)
+    theta = [A0.copy() for _ in range(M)]
+    A, v = A0.copy(), np.zeros(n, np.float32)
+    dp = A0.astype(np.float64)
+    for t in range(5):
+        ups = [on_grid(rng, n, B)[1] for _ in range(M)]
+        sends = [(theta[m] - ups[m]).astype(np.float32) for m in range(M)]   # inner step
+        merges = [s.copy() for s in sends]
+        st, _ = oracle.round_(sends, merges, A, v, B=B, lr=1.0, mu=0.0, alpha=0.0)
+        assert st == 0
+        theta = merges
+        dp = dp - np.mean(np.stack(ups).astype(np.float64), axis=0)
+        for m in range(M):
+            assert np.array_equal(theta[m].astype(np.float64), dp)
+    # with the standard outer optimizer: torch SGD(nesterov) on the averaged
+    # update, one step at a time from the same on-grid anchor and momentum
+    v2 = np.zeros(n, np.float32)
+    for t in range(4):
+        A2, _, _ = on_grid(rng, n, B)
+        ups = [on_grid(rng, n, B)[1] for _ in range(M)]
+        sends = [(A2 - u).astype(np.float32) for u in ups]
+        p = torch.nn.Parameter(torch.from_numpy(A2.copy()))
+        opt = torch.optim.SGD([p], lr=0.4, momentum=0.9, nesterov=True)
+        if t > 0:
+            opt.state[p]["momentum_buffer"] = torch.from_numpy(v2.copy())
+        p.grad = torch.from_numpy(np.mean(np.stack(ups).astype(np.float64), axis=0).astype(np.float32))
+        opt.step()
+        st, _ = oracle.round_(sends, [s.copy() for s in sends], A2, v2, B=B, lr=0.4, mu=0.9, alpha=0.0)
+        assert st == 0
+        ref = p.detach().numpy()
+        assert np.array_equal(bits(opt.state[p]["momentum_buffer"].numpy()), bits(v2))
+        scale = np.maximum.reduce([np.abs(ref), 0.4 * np.abs(p.grad.numpy()), 0.36 * np.abs(v2)])
+        assert np.all(np.abs(ref - A2) <= 16 * 2.0 ** -24 * scale)
+
+
+def test_alpha1_keeps_theta_momentum_advances():
+    rng = np.random.default_rng(21)
+    n = 1100
+    A, D, th = on_grid(rng, n, 1024)
+    m0 = (th - np.float32(2.0 ** -12)).astype(np.float32)
+    merged = [m0.copy()]
+    Aw, v = A.copy(), np.zeros(n, np.float32)
+    oracle.round_([th], merged, Aw, v, B=1024, alpha=1.0)
+    assert np.array_equal(bits(merged[0]), bits(m0)) and v.any() and not np.array_equal(Aw, A)
+
+
+def test_momentum_single_advance_regardless_of_M():
+    """Identical replicas: the mean equals each replica's decoded Delta, so
+    A, v after one round are the same for M = 1 and M = 4."""
+    rng = np.random.default_rng(4)
+    n = 2500
+    A, D, th = on_grid(rng, n, 1024)
+    out = []
+    for M in (1, 4):
+        Aw, v = A.copy(), np.zeros(n, np.float32)
+        oracle.round_([th] * M, [th.copy() for _ in range(M)], Aw, v, B=1024)
+        out.append((bits(Aw).copy(), bits(v).copy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_poisoned_round_is_skipped():
+    n = 2000
+    A = np.ones(n, np.float32)
+    th = [np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    th[1][777] = np.nan
+    merged = [x.copy() for x in th]
+    Aw, v = A.copy(), np.zeros(n, np.float32)
+    st, g = oracle.round_(th, merged, Aw, v)
+    assert st == 1 and np.array_equal(Aw, A) and not v.any()
+
+
+def test_toy_run_streaming_P1_tau0_equals_diloco():
+    """Streaming with P = 1, tau = 0 is Alg. 1 (DiLoCo).  The reference
+    loop below is Alg. 1 written with the oracle's per-round
+    primitives: every H steps quantize, mean, Nesterov, merge with alpha = 0."""
+    import synth
+
+    M, bl, H, T = 2, 3000, 5, 23
+    c = oracle.config(L=1, fs=1, H=H, tau=0, T=T, alpha=0.0)
+    theta, A, v, sent, st = oracle.toy_run(c, M, bl, synth.SEED)
+    assert st == 0
+    n = bl
+    A2 = synth.host_init(synth.flat_segments(n), 0)
+    v2 = np.zeros(n, np.float32)
+    th2 = [A2.copy() for _ in range(M)]
+    for t in range(1, T + 1):
+        for m in range(M):
+            synth.host_apply_toy(th2[m], m, t)
+        if t % H == 0:
+            st2, _ = oracle.round_(th2, th2, A2, v2, B=1024, alpha=0.0)
+            assert st2 == 0
+    for m in range(M):
+        assert np.array_equal(bits(theta[m]), bits(th2[m]))
+    assert np.array_equal(bits(A), bits(A2)) and np.array_equal(bits(v), bits(v2))
+    assert sent == (T // H) * M * oracle.payload_bytes(n, 1024)  # byte accounting
+
+
+def test_toy_config_runs_and_keeps_outer_state_shared():
+    """The toy config of BASELINE.json (M=2, 2^20 params, 2 fragments, H=10,
+    tau=1) runs end to end; byte total = sends x M x payload."""
+    c = oracle.config(L=2, fs=1, H=10, tau=1, T=100)
+    theta, A, v, sent, st = oracle.toy_run(c, 2, 2 ** 19, 250118512)
+    assert st == 0 and np.all(np.isfinite(theta)) and v.any()
+    sends = sum(1 for e in oracle.calendar(c) if e[1] == 0)
+    assert sent == sends * 2 * oracle.payload_bytes(2 ** 19, 1024)
