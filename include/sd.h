@@ -1,0 +1,193 @@
+/* sd.h — C ABI of libsd, the B200-native per-fragment outer synchronization of
+ * Streaming DiLoCo (arXiv 2501.18512).  ABI version 1.
+ *
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n (the reference
+ * paper text and the CPU-program spec written from it); AMB-k = a reading of
+ * the paper recorded in DESIGN.md §2.
+ *
+ * The method (Alg. 2) on one replica m, for one fragment p:
+ *   send step s   (t - t_p) mod H == 0, t >= H        Alg. 2 L6
+ *     Delta_m = A_p - theta_m                           L7  (anchor reading AMB-1)
+ *     4-bit E3M0 codes + fp32 per-block scales
+ *     all-gather of the packed payloads over NVLink     L8
+ *   receive step s + tau                                L10
+ *     wait for the gather                               L11
+ *     g = (1/M) sum_m decode(payload_m), fp32
+ *     v = mu v + g ; A = A - lr (g + mu v)              L12
+ *     theta_m = alpha theta_m + (1 - alpha) A           L13
+ *
+ * Conventions
+ *  - Every function returns sd_status; nothing throws, exits or prints.
+ *    A failing call leaves a message in sd_last_error(ctx) (thread-local
+ *    when ctx == NULL) naming the offending values.
+ *  - Device pointers are CUDA device addresses of the ctx's device, 16-byte
+ *    aligned (256 recommended; gather buffers MUST be 256-byte aligned).
+ *    The caller owns all device memory (theta, anchor, momentum, gather
+ *    buffers) and must keep it alive until the stream work using it is done;
+ *    the library allocates no device memory of its own (NCCL internals
+ *    apart) and writes only slot_out, gather_buf, anchor, momentum, theta.
+ *  - sd_stream is a cudaStream_t (NULL = legacy default stream).  Every
+ *    device call is stream-ordered and asynchronous; errors raised on the
+ *    device (non-finite outer gradients, NCCL async errors) surface at
+ *    sd_check().
+ *  - One sd_ctx per replica (= per GPU process), used from one host thread
+ *    in program order.  The schedule functions are pure and thread-safe.
+ *  - Layout: a fragment is one contiguous fp32 slab of n elements (AMB-18).
+ */
+#ifndef SD_H_
+#define SD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SD_ABI_VERSION 1u
+#define SD_UNIQUE_ID_BYTES 128
+#define SD_PAYLOAD_MAGIC 0x31304453u /* "SD01" little-endian */
+
+typedef struct sd_ctx sd_ctx;
+typedef void* sd_stream; /* cudaStream_t */
+
+typedef enum {
+  SD_OK = 0,
+  SD_ERR_ARG = 1,       /* null / misaligned pointer, n mismatch, wrong slot  */
+  SD_ERR_CONFIG = 2,    /* invalid sd_config (see sd_config_validate)         */
+  SD_ERR_SCHEDULE = 3,  /* fragment p is not scheduled to send/receive at t   */
+  SD_ERR_STATE = 4,     /* call order: merge without sync, p still in flight  */
+  SD_ERR_NONFINITE = 5, /* a replica sent a non-finite outer gradient */
+  SD_ERR_CUDA = 6,
+  SD_ERR_NCCL = 7
+} sd_status;
+
+/* Method configuration.  Defaults (sd_config_default): strided pattern,
+ * embed_policy 0, tau 1, alpha 0.5, outer lr 0.4, momentum 0.9, B 1024. */
+typedef struct {
+  uint32_t abi_version;   /* must be SD_ABI_VERSION                                       */
+  int32_t num_blocks;     /* L: synchronizable blocks (transformer layers), >= 1          */
+  int32_t fragment_size;  /* |p|: blocks per fragment, divides L                 */
+  int32_t pattern;        /* 0 sequential, 1 strided (default)                 */
+  int32_t embed_policy;   /* 0: non-block params join the last fragment             */
+                          /* 1: they form their own extra fragment (reproduces P:501)      */
+  int32_t H;              /* inner steps per round; H >= P                          */
+  int32_t tau;            /* overlap delay, 0 <= tau < H                    */
+  int64_t T;              /* last step: receives due after T are flushed at T;     */
+                          /* 0 = unbounded                                                 */
+  float alpha;            /* merge mix in [0, 1] (default 0.5)        */
+  float outer_lr;         /* Nesterov outer learning rate (0.4), finite             */
+  float outer_momentum;   /* mu in [0, 1) (0.9)                                     */
+  int32_t scale_block;    /* B: elements per fp32 scale; 0 = one scale per fragment        */
+                          /* (SPEC-exact); else a power of two in [256, 2^20]       */
+                          /* (AMB-7; default 1024)                                         */
+} sd_config;
+
+/* ------------------------------------------------------------------------
+ * Host-only, pure: configuration and the fragment scheduler (§8(a) a1).
+ * ---------------------------------------------------------------------- */
+
+/* Fills the defaults listed above for L = num_blocks, |p| = fragment_size, H. */
+sd_status sd_config_default(sd_config* cfg, int32_t num_blocks, int32_t fragment_size, int32_t H);
+
+/* Validates cfg before any work.  On error writes a message naming
+ * the offending values into msg (if msg != NULL, truncated to cap bytes). */
+sd_status sd_config_validate(const sd_config* cfg, char* msg, size_t cap);
+
+/* P: number of fragments = L/|p| (+1 with embed_policy 1). */
+sd_status sd_fragment_count(const sd_config* cfg, int32_t* P);
+
+/* Fragment p: its block indices in ascending order (strided: p, p+P, p+2P, ...;
+ * sequential: p|p| .. (p+1)|p|-1), t_p = floor(p*H/P), and
+ * whether it also holds the non-block (embedding) parameters.
+ * blocks may be NULL (cap 0) to query n_blocks only. */
+sd_status sd_fragment_layout(const sd_config* cfg, int32_t p, int32_t* blocks, int32_t cap,
+                             int32_t* n_blocks, int32_t* t_p, int32_t* holds_embed);
+
+/* The calendar at 1-based step t (Alg. 2 L6 and L10):
+ *   send    = { p : t >= H and (t - t_p) mod H == 0 }
+ *   receive = { p : t - tau >= H and (t - tau - t_p) mod H == 0 }
+ *             plus, at t == T > 0, every p whose send s satisfies T - tau < s <= T.
+ * Both lists ascending, at most cap entries each (cap >= P always suffices). */
+sd_status sd_fragment_schedule(const sd_config* cfg, int64_t t, int32_t* send, int32_t* n_send,
+                               int32_t* recv, int32_t* n_recv, int32_t cap);
+
+/* Scale blocks of a fragment of n elements: 0 if n == 0, 1 if B == 0, else ceil(n/B). */
+int64_t sd_num_scale_blocks(const sd_config* cfg, int64_t n);
+
+/* Bytes of one replica's payload for a fragment of n elements:
+ *   [codes: ceil(n/2) bytes, element 2k in the low nibble of byte k]
+ *   [zero pad to 256]  -> scales offset
+ *   [nb fp32 scales, little endian][zero pad to 16]
+ *   [trailer: u32 magic SD_PAYLOAD_MAGIC, u32 nb, u64 first non-finite index or 2^64-1]
+ *   [zero pad to 256]
+ * Returns 0 on an invalid cfg.  A gather buffer holds M consecutive payloads. */
+size_t sd_payload_bytes(const sd_config* cfg, int64_t n);
+size_t sd_payload_scales_offset(int64_t n);
+size_t sd_payload_trailer_offset(const sd_config* cfg, int64_t n);
+
+/* ------------------------------------------------------------------------
+ * Device context: one per replica = one per GPU.
+ * ---------------------------------------------------------------------- */
+
+/* NCCL unique id for sd_init; rank 0 calls it, the caller broadcasts the
+ * SD_UNIQUE_ID_BYTES bytes (e.g. with torch.distributed). */
+sd_status sd_get_unique_id(uint8_t id[SD_UNIQUE_ID_BYTES]);
+
+/* Creates the context of replica `rank` of M on CUDA device `device`.
+ * id == NULL: no communicator.  Valid for M == 1, and as the single-GPU
+ * emulation seam for M > 1: the caller then fills every slot of the gather
+ * buffer itself (one ctx per emulated replica) and sd_fragment_sync only
+ * orders streams.  id != NULL: collective over the M processes (blocking
+ * NCCL communicator init).  Creates a highest-priority comm stream.  */
+sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, const uint8_t* id,
+                  int32_t device);
+
+/* Outer-state store init (§8(a) a2; AMB-2): anchor <- theta, momentum <- 0. */
+sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, float* momentum,
+                              int64_t n, sd_stream stream);
+
+/* Alg. 2 L7 + E3M0 (§8(a) a3).  p must be scheduled to send at t and not be
+ * in flight.  Reads theta[n], anchor[n]; writes one payload
+ * (sd_payload_bytes) at slot_out, which must be gather_buf + rank * payload
+ * of the buffer later passed to sd_fragment_sync.  A non-finite Delta is
+ * recorded in the payload trailer (index of the first one); the round is
+ * then skipped on every replica and sd_check reports SD_ERR_NONFINITE. */
+sd_status sd_outer_grad_quantize(sd_ctx* ctx, int32_t p, int64_t t, const float* theta,
+                                 const float* anchor, int64_t n, void* slot_out, sd_stream stream);
+
+/* Alg. 2 L8 transport (§8(a) a4): after `stream`'s prior work (the
+ * quantize), an in-place all-gather of the M payloads of gather_buf on the
+ * ctx's comm stream; returns immediately (async-send).  No communicator:
+ * only orders streams. */
+sd_status sd_fragment_sync(sd_ctx* ctx, int32_t p, int64_t t, void* gather_buf, int64_t n,
+                           sd_stream stream);
+
+/* Alg. 2 L11-13 (§8(a) a5 + a6): `stream` waits for the gather of p
+ * (block-receive), then one fused kernel: decode + M-way fp32 mean in
+ * ascending replica order, Nesterov on (anchor, momentum), alpha-merge into
+ * theta (the live parameters after tau inner steps).  p must be received at
+ * t (send step + tau, or the flush at T).  If any payload is poisoned or
+ * malformed, nothing is written (identically on every replica). */
+sd_status sd_merge(sd_ctx* ctx, int32_t p, int64_t t, const void* gather_buf, float* theta,
+                   float* anchor, float* momentum, int64_t n, sd_stream stream);
+
+/* Synchronizes the device and reports deferred errors: CUDA errors, NCCL
+ * async errors, and a skipped (poisoned) round — then SD_ERR_NONFINITE and
+ * *first_bad_index (if non-NULL) = index of the first non-finite Delta. */
+sd_status sd_check(sd_ctx* ctx, int64_t* first_bad_index);
+
+/* Message of the last failing call on ctx (thread-local one if ctx == NULL). */
+const char* sd_last_error(const sd_ctx* ctx);
+
+/* Destroys the communicator, streams and events.  NULL is a no-op. */
+sd_status sd_finalize(sd_ctx* ctx);
+
+/* Number of kernels libsd has launched in this process (for bench.py's
+ * gpu_launches accounting). */
+uint64_t sd_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SD_H_ */

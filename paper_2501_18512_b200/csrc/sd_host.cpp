@@ -1,0 +1,483 @@
+// sd_host.cpp — libsd host side: config validation, the closed-form fragment
+// scheduler, the per-replica context (NCCL communicator, comm stream, events,
+// in-flight table) and the C ABI of include/sd.h.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "sd.h"
+#include "sd_kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+std::atomic<uint64_t> g_launches{0};
+
+sd_status fail(char* buf, sd_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, 512, fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// Full validation (config is validated before any work).  Messages
+// name the offending values.
+sd_status validate(const sd_config* c, char* msg, size_t cap) {
+  char tmp[512];
+  sd_status st = SD_OK;
+  if (!c) {
+    st = fail(tmp, SD_ERR_ARG, "config pointer is NULL");
+  } else if (c->abi_version != SD_ABI_VERSION) {
+    st = fail(tmp, SD_ERR_CONFIG, "abi_version %u != SD_ABI_VERSION %u", c->abi_version, SD_ABI_VERSION);
+  } else if (c->num_blocks < 1 || c->fragment_size < 1) {
+    st = fail(tmp, SD_ERR_CONFIG, "num_blocks %d and fragment_size %d must both be >= 1", c->num_blocks,
+              c->fragment_size);
+  } else if (c->num_blocks % c->fragment_size != 0) {
+    st = fail(tmp, SD_ERR_CONFIG, "fragment_size %d does not divide num_blocks %d", c->fragment_size,
+              c->num_blocks);
+  } else if (c->pattern != 0 && c->pattern != 1) {
+    st = fail(tmp, SD_ERR_CONFIG, "pattern %d is neither 0 (sequential) nor 1 (strided)", c->pattern);
+  } else if (c->embed_policy != 0 && c->embed_policy != 1) {
+    st = fail(tmp, SD_ERR_CONFIG, "embed_policy %d is neither 0 nor 1", c->embed_policy);
+  } else {
+    const int32_t P = c->num_blocks / c->fragment_size + (c->embed_policy == 1 ? 1 : 0);
+    if (c->H < 1 || c->H < P) {
+      st = fail(tmp, SD_ERR_CONFIG, "H %d must be >= 1 and >= the number of fragments P %d", c->H, P);
+    } else if (c->tau < 0 || c->tau >= c->H) {
+      st = fail(tmp, SD_ERR_CONFIG, "tau %d violates 0 <= tau < H (H = %d)", c->tau, c->H);
+    } else if (c->T < 0) {
+      st = fail(tmp, SD_ERR_CONFIG, "T %lld must be >= 0 (0 = unbounded)", (long long)c->T);
+    } else if (!(c->alpha >= 0.0f && c->alpha <= 1.0f)) {
+      st = fail(tmp, SD_ERR_CONFIG, "alpha %g is not in [0, 1]", (double)c->alpha);
+    } else if (!(c->outer_lr == c->outer_lr) || c->outer_lr > 3.4e38f || c->outer_lr < -3.4e38f) {
+      st = fail(tmp, SD_ERR_CONFIG, "outer_lr %g is not finite", (double)c->outer_lr);
+    } else if (!(c->outer_momentum >= 0.0f && c->outer_momentum < 1.0f)) {
+      st = fail(tmp, SD_ERR_CONFIG, "outer_momentum %g is not in [0, 1)", (double)c->outer_momentum);
+    } else if (c->scale_block != 0 &&
+               (!is_pow2(c->scale_block) || c->scale_block < 256 || c->scale_block > (1 << 20))) {
+      st = fail(tmp, SD_ERR_CONFIG, "scale_block %d is neither 0 nor a power of two in [256, 1048576]",
+                c->scale_block);
+    }
+  }
+  if (st != SD_OK) {
+    snprintf(g_err, sizeof g_err, "%s", tmp);
+    if (msg && cap) snprintf(msg, cap, "%s", tmp);
+  }
+  return st;
+}
+
+int32_t num_fragments(const sd_config* c) {
+  return c->num_blocks / c->fragment_size + (c->embed_policy == 1 ? 1 : 0);
+}
+
+int32_t offset_of(const sd_config* c, int32_t p) {  // t_p = floor(p H / P)
+  return (int32_t)(((int64_t)p * c->H) / num_fragments(c));
+}
+
+// (t - t_p) mod H == 0 with t >= H  (Alg. 2 L6; first send S:73)
+bool sends_at(const sd_config* c, int32_t p, int64_t t) {
+  return t >= c->H && (t - offset_of(c, p)) % c->H == 0;
+}
+
+// the send step s whose receive falls at t, or 0 (Alg. 2 L10; flush S:322)
+int64_t receive_send_step(const sd_config* c, int32_t p, int64_t t) {
+  if (c->T > 0 && t > c->T) return 0;
+  const int64_t s = t - c->tau;
+  if (s >= 1 && sends_at(c, p, s)) return s;
+  if (c->T > 0 && t == c->T) {  // flush: the send of p in (T - tau, T], if any
+    for (int64_t q = c->T - c->tau + 1; q <= c->T; ++q)
+      if (q >= 1 && sends_at(c, p, q)) return q;
+  }
+  return 0;
+}
+
+sdk::Payload payload_of(const sd_config* c, int64_t n) {
+  sdk::Payload pl;
+  pl.n = n;
+  pl.B = c->scale_block;
+  pl.nb = n == 0 ? 0 : (c->scale_block == 0 ? 1 : (n + c->scale_block - 1) / c->scale_block);
+  pl.scales_off = (size_t)align_up((n + 1) / 2, 256);
+  pl.trailer_off = pl.scales_off + (size_t)align_up(4 * pl.nb, 16);
+  pl.bytes = pl.scales_off + (size_t)align_up(align_up(4 * pl.nb, 16) + 16, 256);
+  return pl;
+}
+
+enum FragState { IDLE = 0, QUANTIZED = 1, SYNCED = 2 };
+
+struct Inflight {
+  FragState state = IDLE;
+  int64_t send_step = 0;
+  int64_t n = 0;
+  const void* slot = nullptr;
+  const void* gather = nullptr;
+};
+
+}  // namespace
+
+struct sd_ctx {
+  sd_config cfg;
+  int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<Inflight> fl;
+  unsigned long long* status_host = nullptr;  // {first_bad, flags}: pinned, mapped
+  unsigned long long* status_dev = nullptr;
+  char err[512] = "";
+};
+
+namespace {
+
+sd_status cuda_fail(sd_ctx* c, cudaError_t e, const char* what) {
+  snprintf(g_err, sizeof g_err, "%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+  if (c) snprintf(c->err, sizeof c->err, "%s", g_err);
+  return SD_ERR_CUDA;
+}
+
+sd_status ctx_fail(sd_ctx* c, sd_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(c->err, sizeof c->err, fmt, ap);
+  va_end(ap);
+  snprintf(g_err, sizeof g_err, "%s", c->err);
+  return st;
+}
+
+#define SD_CUDA(ctx, call)                              \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+sd_status check_ptr(sd_ctx* c, const void* ptr, size_t align, const char* name) {
+  if (!ptr) return ctx_fail(c, SD_ERR_ARG, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(ptr) % align != 0)
+    return ctx_fail(c, SD_ERR_ARG, "%s = %p is not %zu-byte aligned", name, ptr, align);
+  return SD_OK;
+}
+
+sd_status check_fragment(sd_ctx* c, int32_t p, int64_t t, int64_t n) {
+  if (p < 0 || p >= c->P) return ctx_fail(c, SD_ERR_ARG, "fragment %d out of range [0, %d)", p, c->P);
+  if (t < 1) return ctx_fail(c, SD_ERR_ARG, "step t = %lld must be >= 1 (1-based, S:323)", (long long)t);
+  if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
+  return SD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sd_status sd_config_default(sd_config* c, int32_t num_blocks, int32_t fragment_size, int32_t H) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "config pointer is NULL");
+  c->abi_version = SD_ABI_VERSION;
+  c->num_blocks = num_blocks;
+  c->fragment_size = fragment_size;
+  c->pattern = 1;
+  c->embed_policy = 0;
+  c->H = H;
+  c->tau = 1;
+  c->T = 0;
+  c->alpha = 0.5f;
+  c->outer_lr = 0.4f;
+  c->outer_momentum = 0.9f;
+  c->scale_block = 1024;
+  return SD_OK;
+}
+
+sd_status sd_config_validate(const sd_config* cfg, char* msg, size_t cap) {
+  if (msg && cap) msg[0] = 0;
+  return validate(cfg, msg, cap);
+}
+
+sd_status sd_fragment_count(const sd_config* cfg, int32_t* P) {
+  sd_status st = validate(cfg, nullptr, 0);
+  if (st != SD_OK) return st;
+  if (!P) return fail(g_err, SD_ERR_ARG, "P pointer is NULL");
+  *P = num_fragments(cfg);
+  return SD_OK;
+}
+
+sd_status sd_fragment_layout(const sd_config* cfg, int32_t p, int32_t* blocks, int32_t cap,
+                             int32_t* n_blocks, int32_t* t_p, int32_t* holds_embed) {
+  sd_status st = validate(cfg, nullptr, 0);
+  if (st != SD_OK) return st;
+  const int32_t P = num_fragments(cfg);
+  const int32_t Pb = cfg->num_blocks / cfg->fragment_size;
+  if (p < 0 || p >= P) return fail(g_err, SD_ERR_ARG, "fragment %d out of range [0, %d)", p, P);
+  const int32_t nbk = p < Pb ? cfg->fragment_size : 0;
+  if (blocks && cap < nbk) return fail(g_err, SD_ERR_ARG, "cap %d < %d blocks of fragment %d", cap, nbk, p);
+  if (blocks)
+    for (int32_t k = 0; k < nbk; ++k) blocks[k] = cfg->pattern == 0 ? p * cfg->fragment_size + k : p + k * Pb;
+  if (n_blocks) *n_blocks = nbk;
+  if (t_p) *t_p = offset_of(cfg, p);
+  if (holds_embed) *holds_embed = (cfg->embed_policy == 0) ? (p == Pb - 1) : (p == Pb);
+  return SD_OK;
+}
+
+sd_status sd_fragment_schedule(const sd_config* cfg, int64_t t, int32_t* send, int32_t* n_send,
+                               int32_t* recv, int32_t* n_recv, int32_t cap) {
+  sd_status st = validate(cfg, nullptr, 0);
+  if (st != SD_OK) return st;
+  if (t < 1) return fail(g_err, SD_ERR_ARG, "step t = %lld must be >= 1 (1-based, S:323)", (long long)t);
+  if (!n_send || !n_recv) return fail(g_err, SD_ERR_ARG, "n_send / n_recv pointer is NULL");
+  const int32_t P = num_fragments(cfg);
+  int32_t ns = 0, nr = 0;
+  for (int32_t p = 0; p < P; ++p) {
+    if ((cfg->T == 0 || t <= cfg->T) && sends_at(cfg, p, t)) {
+      if (ns >= cap || !send) return fail(g_err, SD_ERR_ARG, "send list capacity %d too small", cap);
+      send[ns++] = p;
+    }
+  }
+  for (int32_t p = 0; p < P; ++p) {
+    if (receive_send_step(cfg, p, t) != 0) {
+      if (nr >= cap || !recv) return fail(g_err, SD_ERR_ARG, "receive list capacity %d too small", cap);
+      recv[nr++] = p;
+    }
+  }
+  *n_send = ns;
+  *n_recv = nr;
+  return SD_OK;
+}
+
+int64_t sd_num_scale_blocks(const sd_config* cfg, int64_t n) {
+  if (validate(cfg, nullptr, 0) != SD_OK || n < 0) return 0;
+  return payload_of(cfg, n).nb;
+}
+
+size_t sd_payload_bytes(const sd_config* cfg, int64_t n) {
+  if (validate(cfg, nullptr, 0) != SD_OK || n < 0) return 0;
+  return payload_of(cfg, n).bytes;
+}
+
+size_t sd_payload_scales_offset(int64_t n) { return n < 0 ? 0 : (size_t)align_up((n + 1) / 2, 256); }
+
+size_t sd_payload_trailer_offset(const sd_config* cfg, int64_t n) {
+  if (validate(cfg, nullptr, 0) != SD_OK || n < 0) return 0;
+  return payload_of(cfg, n).trailer_off;
+}
+
+sd_status sd_get_unique_id(uint8_t id[SD_UNIQUE_ID_BYTES]) {
+  if (!id) return fail(g_err, SD_ERR_ARG, "id pointer is NULL");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(g_err, SD_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(u.internal) == SD_UNIQUE_ID_BYTES, "NCCL unique id size");
+  memcpy(id, u.internal, SD_UNIQUE_ID_BYTES);
+  return SD_OK;
+}
+
+sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, const uint8_t* id,
+                  int32_t device) {
+  if (!out) return fail(g_err, SD_ERR_ARG, "out pointer is NULL");
+  *out = nullptr;
+  sd_status st = validate(cfg, nullptr, 0);
+  if (st != SD_OK) return st;
+  if (M < 1 || rank < 0 || rank >= M) return fail(g_err, SD_ERR_ARG, "rank %d / M %d: need 0 <= rank < M", rank, M);
+  sd_ctx* c = new (std::nothrow) sd_ctx();
+  if (!c) return fail(g_err, SD_ERR_ARG, "out of host memory");
+  c->cfg = *cfg;
+  c->rank = rank;
+  c->M = M;
+  c->device = device;
+  c->P = num_fragments(cfg);
+  c->fl.resize((size_t)c->P);
+  auto bail = [&](sd_status s) {
+    sd_finalize(c);
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaSetDevice"));
+  e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaDeviceGetAttribute"));
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  e = cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreateWithPriority"));
+  c->ready.assign((size_t)c->P, nullptr);
+  c->done.assign((size_t)c->P, nullptr);
+  for (int32_t p = 0; p < c->P; ++p) {
+    e = cudaEventCreateWithFlags(&c->ready[p], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaEventCreate"));
+  }
+  e = cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), 2 * sizeof(unsigned long long), cudaHostAllocMapped);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaHostAlloc(status)"));
+  c->status_host[0] = ~0ull;
+  c->status_host[1] = 0;
+  e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->status_dev), c->status_host, 0);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaHostGetDevicePointer"));
+  if (id && M > 1) {
+    ncclUniqueId u;
+    memcpy(u.internal, id, SD_UNIQUE_ID_BYTES);
+    ncclResult_t r = ncclCommInitRank(&c->comm, M, u, rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      fail(g_err, SD_ERR_NCCL, "ncclCommInitRank(M=%d, rank=%d): %s", M, rank, ncclGetErrorString(r));
+      return bail(SD_ERR_NCCL);
+    }
+  }
+  *out = c;
+  return SD_OK;
+}
+
+sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, float* momentum, int64_t n,
+                              sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
+  if (n == 0) return SD_OK;
+  sd_status st;
+  if ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")) ||
+      (st = check_ptr(c, momentum, 16, "momentum")))
+    return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  if (anchor != theta) SD_CUDA(c, cudaMemcpyAsync(anchor, theta, 4 * (size_t)n, cudaMemcpyDeviceToDevice, s));
+  SD_CUDA(c, cudaMemsetAsync(momentum, 0, 4 * (size_t)n, s));
+  return SD_OK;
+}
+
+sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor,
+                                 int64_t n, void* slot_out, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, t, n))) return st;
+  if ((c->cfg.T == 0 || t <= c->cfg.T) ? !sends_at(&c->cfg, p, t) : true)
+    return ctx_fail(c, SD_ERR_SCHEDULE, "fragment %d is not scheduled to send at step %lld (t_p = %d, H = %d)", p,
+                    (long long)t, offset_of(&c->cfg, p), c->cfg.H);
+  if (c->fl[p].state != IDLE)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d is still in flight (sent at step %lld)", p,
+                    (long long)c->fl[p].send_step);
+  if ((st = check_ptr(c, slot_out, 256, "slot_out"))) return st;
+  if (n > 0 && ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")))) return st;
+  const sdk::Payload pl = payload_of(&c->cfg, n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  uint8_t* slot = static_cast<uint8_t*>(slot_out);
+  SD_CUDA(c, cudaMemsetAsync(slot + pl.trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64 - 1
+  const int k = sdk::launch_quantize(theta, anchor, pl, slot, c->num_sms, s);
+  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
+  g_launches += (uint64_t)k;
+  c->fl[p].state = QUANTIZED;
+  c->fl[p].send_step = t;
+  c->fl[p].n = n;
+  c->fl[p].slot = slot_out;
+  return SD_OK;
+}
+
+sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, int64_t n, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, t, n))) return st;
+  Inflight& f = c->fl[p];
+  if (f.state != QUANTIZED || f.send_step != t)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d: sync at step %lld without a quantize at that step", p, (long long)t);
+  if (f.n != n) return ctx_fail(c, SD_ERR_ARG, "fragment %d: n = %lld but quantized n = %lld", p, (long long)n, (long long)f.n);
+  if ((st = check_ptr(c, gather_buf, 256, "gather_buf"))) return st;
+  const sdk::Payload pl = payload_of(&c->cfg, n);
+  uint8_t* g = static_cast<uint8_t*>(gather_buf);
+  if (f.slot != g + (size_t)c->rank * pl.bytes)
+    return ctx_fail(c, SD_ERR_ARG, "slot_out %p != gather_buf + rank * payload (%p + %d * %zu)", f.slot, gather_buf,
+                    c->rank, pl.bytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  if (c->comm) {
+    SD_CUDA(c, cudaEventRecord(c->ready[p], s));
+    SD_CUDA(c, cudaStreamWaitEvent(c->comm_stream, c->ready[p], 0));
+    ncclResult_t r = ncclAllGather(g + (size_t)c->rank * pl.bytes, g, pl.bytes, ncclUint8, c->comm, c->comm_stream);
+    if (r != ncclSuccess) return ctx_fail(c, SD_ERR_NCCL, "ncclAllGather(fragment %d): %s", p, ncclGetErrorString(r));
+    SD_CUDA(c, cudaEventRecord(c->done[p], c->comm_stream));
+  } else {
+    SD_CUDA(c, cudaEventRecord(c->done[p], s));
+  }
+  f.state = SYNCED;
+  f.gather = gather_buf;
+  return SD_OK;
+}
+
+sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
+                   float* momentum, int64_t n, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, t, n))) return st;
+  const int64_t s_step = receive_send_step(&c->cfg, p, t);
+  if (s_step == 0)
+    return ctx_fail(c, SD_ERR_SCHEDULE, "fragment %d is not scheduled to be received at step %lld (tau = %d)", p,
+                    (long long)t, c->cfg.tau);
+  Inflight& f = c->fl[p];
+  if (f.state != SYNCED || f.send_step != s_step)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d: merge at step %lld needs the sync of step %lld first", p,
+                    (long long)t, (long long)s_step);
+  if (f.n != n) return ctx_fail(c, SD_ERR_ARG, "fragment %d: n = %lld but synced n = %lld", p, (long long)n, (long long)f.n);
+  if (f.gather != gather_buf)
+    return ctx_fail(c, SD_ERR_ARG, "fragment %d: gather_buf %p is not the synced buffer %p", p, gather_buf, f.gather);
+  if (n > 0 && ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")) ||
+                (st = check_ptr(c, momentum, 16, "momentum"))))
+    return st;
+  const sdk::Payload pl = payload_of(&c->cfg, n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
+  const int k = sdk::launch_apply(static_cast<const uint8_t*>(gather_buf), pl, c->M, theta, anchor, momentum,
+                                  c->cfg.outer_lr, c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s);
+  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_apply launch");
+  g_launches += (uint64_t)k;
+  f = Inflight();
+  return SD_OK;
+}
+
+sd_status sd_check(sd_ctx* c, int64_t* first_bad_index) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (first_bad_index) *first_bad_index = -1;
+  SD_CUDA(c, cudaSetDevice(c->device));
+  SD_CUDA(c, cudaDeviceSynchronize());
+  if (c->comm) {
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c->comm, &ar);
+    if (r != ncclSuccess || ar != ncclSuccess)
+      return ctx_fail(c, SD_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(r != ncclSuccess ? r : ar));
+  }
+  volatile unsigned long long* h = c->status_host;
+  const unsigned long long flags = h[1], fb = h[0];
+  if (flags != 0) {
+    h[0] = ~0ull;
+    h[1] = 0;
+    if (first_bad_index) *first_bad_index = fb == ~0ull ? -1 : (int64_t)fb;
+    if (flags == 2) return ctx_fail(c, SD_ERR_STATE, "a gather slot had no valid payload trailer; round skipped");
+    return ctx_fail(c, SD_ERR_NONFINITE, "non-finite outer gradient at fragment index %llu; round skipped", fb);
+  }
+  return SD_OK;
+}
+
+const char* sd_last_error(const sd_ctx* c) { return c ? c->err : g_err; }
+
+sd_status sd_finalize(sd_ctx* c) {
+  if (!c) return SD_OK;
+  cudaSetDevice(c->device);
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  for (cudaEvent_t e : c->ready)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->done)
+    if (e) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->status_host) cudaFreeHost(c->status_host);
+  delete c;
+  return SD_OK;
+}
+
+uint64_t sd_kernel_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

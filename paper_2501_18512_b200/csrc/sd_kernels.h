@@ -1,0 +1,31 @@
+// sd_kernels.h — launchers of libsd's sm_100a kernels (internal to libsd).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sdk {
+
+struct Payload {          // byte offsets inside one replica payload (sd.h)
+  int64_t n;              // fragment elements
+  int64_t nb;             // scale blocks
+  int32_t B;              // elements per scale block (0 = whole fragment)
+  size_t scales_off;      // align256(ceil(n/2))
+  size_t trailer_off;     // scales_off + align16(4 nb)
+  size_t bytes;           // total payload bytes
+};
+
+// Delta = anchor - theta, per-block absmax, exact E3M0, nibble pack, trailer.
+// slot: one payload (256-aligned).  The trailer's first_bad word must hold
+// 2^64-1 before the launch (sd_outer_grad_quantize memsets it).
+// Returns the number of kernels launched, or -1 on a launch error.
+int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot,
+                    int num_sms, cudaStream_t st);
+
+// Fused decode + M-way fp32 mean + Nesterov + anchor update + alpha-merge.
+// status: host-mapped pinned word pair {first_bad, flags} written when the
+// round is skipped.  Returns kernels launched or -1.
+int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor,
+                 float* momentum, float lr, float mu, float alpha, unsigned long long* status,
+                 int num_sms, cudaStream_t st);
+
+}  // namespace sdk

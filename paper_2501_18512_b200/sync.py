@@ -1,0 +1,65 @@
+"""FragmentSync: one replica's side of Alg. 2's outer synchronization.
+
+Owns the libsd context and the per-fragment gather buffers (torch device
+memory) and issues the C-ABI calls in the paper's order at a step t:
+sends first (Alg. 2 L6-8: sd_outer_grad_quantize + sd_fragment_sync), then
+receives (L10-13: sd_merge).  torch supplies memory, streams and the
+process group that broadcasts the NCCL unique id; nothing here computes.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import sd
+
+
+class FragmentSync:
+    def __init__(self, cfg: sd.SdConfig, frag_numel, rank: int = 0, world: int = 1, device: int = 0,
+                 unique_id: bytes | None = None):
+        self.cfg = cfg
+        self.rank, self.world, self.device = rank, world, device
+        self.P = sd.sd_fragment_count(cfg)
+        if len(frag_numel) != self.P:
+            raise ValueError(f"{len(frag_numel)} fragment sizes given, the config has P = {self.P}")
+        self.n = [int(x) for x in frag_numel]
+        if world > 1 and unique_id is None:
+            import torch.distributed as dist
+
+            obj = [sd.sd_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            unique_id = obj[0]
+        self.ctx = sd.SdContext(cfg, rank, world, unique_id if world > 1 else None, device)
+        self.payload = [sd.sd_payload_bytes(cfg, n) for n in self.n]
+        dev = torch.device("cuda", device)
+        self.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in self.payload]
+
+    def slot(self, p: int) -> torch.Tensor:
+        pb = self.payload[p]
+        return self.gather[p][self.rank * pb:(self.rank + 1) * pb]
+
+    def outer_state_init(self, p, theta, anchor, momentum, stream=None):
+        self.ctx.sd_outer_state_init(theta, anchor, momentum, self.n[p], stream)
+
+    def send(self, p, t, theta, anchor, stream=None):
+        """Alg. 2 L7-8: Delta + E3M0 into this replica's slot, then the async all-gather."""
+        self.ctx.sd_outer_grad_quantize(p, t, theta, anchor, self.slot(p), self.n[p], stream)
+        self.ctx.sd_fragment_sync(p, t, self.gather[p], self.n[p], stream)
+
+    def receive(self, p, t, theta, anchor, momentum, stream=None):
+        """Alg. 2 L11-13: block-receive, mean, Nesterov, alpha-merge (one fused kernel)."""
+        self.ctx.sd_merge(p, t, self.gather[p], theta, anchor, momentum, self.n[p], stream)
+
+    def step(self, t, theta, anchor, momentum, stream=None):
+        """All calendar events of step t (after the inner step); lists indexed by fragment."""
+        send, recv = sd.sd_fragment_schedule(self.cfg, t)
+        for p in send:
+            self.send(p, t, theta[p], anchor[p], stream)
+        for p in recv:
+            self.receive(p, t, theta[p], anchor[p], momentum[p], stream)
+        return send, recv
+
+    def check(self):
+        return self.ctx.sd_check()
+
+    def close(self):
+        self.ctx.sd_finalize()

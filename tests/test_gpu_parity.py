@@ -1,0 +1,310 @@
+"""GPU parity: libsd's CUDA path (through the C ABI) vs the CPU oracle.
+
+Bar: payload bytes (codes, scales, padding, trailer) are
+byte-identical; anchor, momentum and live parameters are bit-identical
+(0 differing elements is the expectation under the pinned fp32 operation
+sequence), with the floored 1e-6 relative check of BASELINE.json's
+north_star as the stated tolerance.  Inputs: seeded synthetic data shaped
+like the paper's Chinchilla fragments (synth/) plus codec edge cases."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2501_18512_b200 import sd
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from gpu_harness import DEV, EmulatedReplicas, bits, edge_deltas, theta_anchor_for, to_dev
+
+
+def floored_rel_err(gpu: np.ndarray, ora: np.ndarray) -> float:
+    """max_i |g_i - o_i| / max(|o_i|, 2^-10 max_j |o_j|)"""
+    g, o = gpu.astype(np.float64), ora.astype(np.float64)
+    if o.size == 0:
+        return 0.0
+    floor = 2.0 ** -10 * np.max(np.abs(o))
+    den = np.maximum(np.abs(o), floor)
+    den[den == 0] = 1.0
+    return float(np.max(np.abs(g - o) / den))
+
+
+def assert_same(gpu, ora, what):
+    gb, ob = bits(gpu), bits(ora)
+    nbad = int(np.count_nonzero(gb != ob))
+    assert floored_rel_err(gpu if isinstance(gpu, np.ndarray) else gpu.cpu().numpy(), ora) <= 1e-6, what
+    assert nbad == 0, f"{what}: {nbad} elements differ bitwise"
+
+
+def cfg_for(B, alpha=0.5, lr=0.4, mu=0.9, tau=1):
+    return sd.sd_config_default(2, 1, 10, tau=tau, scale_block=B, alpha=alpha, outer_lr=lr, outer_momentum=mu)
+
+
+# ------------------------------------------------------------------ quantize
+@pytest.mark.parametrize("B", [0, 256, 512, 1024, 2048, 65536])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 1023, 1024, 1025, 4097, 33 * 1024 + 511, 262144 + 3])
+def test_quantize_payload_bytes_match(n, B):
+    rng = np.random.default_rng(n * 7 + B)
+    cfg = cfg_for(B)
+    for exact in (True, False):
+        delta = edge_deltas(n, B, rng)
+        A, th = theta_anchor_for(delta, rng, exact)
+        rep = EmulatedReplicas(cfg, 1, n)
+        rep.slot(0).fill_(0xAB)  # garbage: every byte must be written
+        rep.quantize_all(0, 10, [to_dev(th)], [to_dev(A)])
+        torch.cuda.synchronize()
+        want, poisoned = oracle.quantize(th, A, B)
+        got = rep.gather.cpu().numpy()
+        assert not poisoned
+        diff = np.nonzero(got != want)[0]
+        assert diff.size == 0, f"n={n} B={B} exact={exact}: {diff.size} bytes differ, first at {diff[:8]}"
+        rep.close()
+
+
+def test_quantize_synthetic_chinchilla_fragment():
+    segs = synth.fragment_segments(128, [0, 5], with_embed=True, vocab=1000)
+    n = synth.segments_numel(segs)
+    A = synth.host_init(segs, 3)
+    th = synth.host_apply_window(A.copy(), segs, 3, 1, 1)
+    for B in (1024, 0):
+        rep = EmulatedReplicas(cfg_for(B), 1, n)
+        rep.quantize_all(0, 10, [to_dev(th)], [to_dev(A)])
+        torch.cuda.synchronize()
+        want, _ = oracle.quantize(th, A, B)
+        assert np.array_equal(rep.gather.cpu().numpy(), want)
+        rep.close()
+
+
+# -------------------------------------------------------------- full rounds
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("B", [1024, 256, 0])
+def test_rounds_bit_exact(M, B):
+    """R = 3 rounds of one fragment on M emulated replicas: payloads, anchor,
+    momentum and every replica's merged parameters vs or_round."""
+    segs = synth.fragment_segments(64, [0, 2], with_embed=False)
+    n = synth.segments_numel(segs) + 123  # ragged: not a multiple of 4 or of B
+    segs = np.concatenate([segs, np.array([(n - 123, 123, synth.NORM, 0, 1, 0)], dtype=synth.SEG_DTYPE)])
+    p, H, tau = 0, 10, 1
+    cfg = cfg_for(B, tau=tau)
+    A_o = synth.host_init(segs, p)
+    v_o = np.zeros(n, np.float32)
+    th_o = [A_o.copy() for _ in range(M)]
+    rep = EmulatedReplicas(cfg, M, n)
+    A_d = [to_dev(A_o) for _ in range(M)]
+    v_d = [torch.zeros(n, dtype=torch.float32, device=DEV) for _ in range(M)]
+    th_d = [to_dev(A_o) for _ in range(M)]
+    for r in range(1, 4):
+        t_send = r * H
+        for m in range(M):
+            synth.host_apply_window(th_o[m], segs, p, m, r)
+            synth.dev_apply_window(th_d[m], segs, p, m, r)
+        rep.quantize_all(p, t_send, th_d, A_d)
+        sends = [x.copy() for x in th_o]
+        for m in range(M):
+            synth.host_apply_drift(th_o[m], segs, p, m, r)
+            synth.dev_apply_drift(th_d[m], segs, p, m, r)
+        rep.merge_all(p, t_send + tau, th_d, A_d, v_d)
+        st, g_o = oracle.round_(sends, th_o, A_o, v_o, B=B)
+        torch.cuda.synchronize()
+        assert st == 0
+        assert np.array_equal(rep.gather.cpu().numpy(), g_o), f"round {r}: gather bytes differ"
+        for m in range(M):
+            assert_same(A_d[m], A_o, f"round {r} anchor (replica {m})")
+            assert_same(v_d[m], v_o, f"round {r} momentum (replica {m})")
+            assert_same(th_d[m], th_o[m], f"round {r} theta (replica {m})")
+    assert all(s == (sd.SD_OK, -1) for s in rep.check_all())
+    rep.close()
+
+
+@pytest.mark.parametrize("alpha,lr,mu", [(0.0, 1.0, 0.0), (1.0, 0.4, 0.9), (0.25, 0.7, 0.5)])
+def test_rounds_hyperparameter_edges(alpha, lr, mu):
+    rng = np.random.default_rng(int(alpha * 100 + lr * 10))
+    n, M = 8192 + 5, 2
+    cfg = cfg_for(1024, alpha=alpha, lr=lr, mu=mu)
+    A0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    sends = [(A0 - edge_deltas(n, 1024, rng)).astype(np.float32) for _ in range(M)]
+    merges = [(s - np.float32(1e-4)).astype(np.float32) for s in sends]
+    rep = EmulatedReplicas(cfg, M, n)
+    A_d, v_d = [to_dev(A0) for _ in range(M)], [torch.full((n,), 0.01, device=DEV) for _ in range(M)]
+    th_d = [to_dev(s) for s in sends]
+    rep.quantize_all(0, 10, th_d, A_d)
+    for m in range(M):
+        th_d[m].copy_(to_dev(merges[m]))
+    rep.merge_all(0, 11, th_d, A_d, v_d)
+    A_o, v_o = A0.copy(), np.full(n, 0.01, np.float32)
+    mo = [x.copy() for x in merges]
+    oracle.round_(sends, mo, A_o, v_o, B=1024, lr=lr, mu=mu, alpha=alpha)
+    torch.cuda.synchronize()
+    for m in range(M):
+        assert_same(A_d[m], A_o, "anchor")
+        assert_same(v_d[m], v_o, "momentum")
+        assert_same(th_d[m], mo[m], "theta")
+    rep.close()
+
+
+def test_empty_fragment():
+    cfg = cfg_for(1024)
+    rep = EmulatedReplicas(cfg, 2, 0)
+    e = torch.empty(0, device=DEV)
+    rep.quantize_all(0, 10, [e, e], [e, e])
+    rep.merge_all(0, 11, [e, e], [e, e], [e, e])
+    torch.cuda.synchronize()
+    want, _ = oracle.quantize(np.zeros(0, np.float32), np.zeros(0, np.float32), 1024)
+    assert np.array_equal(rep.gather.cpu().numpy(), np.concatenate([want, want]))
+    rep.close()
+
+
+# ------------------------------------------------------------------- poison
+def test_nonfinite_round_skipped_on_every_replica():
+    n, M = 5000, 2
+    cfg = cfg_for(1024)
+    rep = EmulatedReplicas(cfg, M, n)
+    A0 = np.ones(n, np.float32)
+    th = [np.zeros(n, np.float32) for _ in range(M)]
+    th[1][4321] = np.inf
+    th[1][2222] = np.nan
+    A_d = [to_dev(A0) for _ in range(M)]
+    v_d = [torch.zeros(n, device=DEV) for _ in range(M)]
+    th_d = [to_dev(x) for x in th]
+    rep.quantize_all(0, 10, th_d, A_d)
+    rep.merge_all(0, 11, th_d, A_d, v_d)
+    torch.cuda.synchronize()
+    r, fb = oracle.payload_poisoned(rep.gather.cpu().numpy()[rep.pb:], n, 1024)
+    assert r == 1 and fb == 2222
+    for m in range(M):
+        assert np.array_equal(A_d[m].cpu().numpy(), A0) and not v_d[m].any()
+        assert np.array_equal(bits(th_d[m]), bits(th[m]))
+    for st in rep.check_all():
+        assert st == (sd.SD_ERR_NONFINITE, 2222)
+    rep.close()
+
+
+# -------------------------------------------------------- call-order checks
+def test_schedule_and_state_errors():
+    n = 4096
+    cfg = cfg_for(1024)
+    rep = EmulatedReplicas(cfg, 2, n)
+    x = torch.zeros(n, device=DEV)
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[0].sd_outer_grad_quantize(0, 11, x, x, rep.slot(0), n)  # fragment 0 sends at 10, 20, ...
+    assert e.value.status == sd.SD_ERR_SCHEDULE
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[0].sd_merge(0, 11, rep.gather, x, x, x, n)  # nothing in flight
+    assert e.value.status == sd.SD_ERR_STATE
+    rep.ctx[0].sd_outer_grad_quantize(0, 10, x, x, rep.slot(0), n)
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[0].sd_outer_grad_quantize(0, 10, x, x, rep.slot(0), n)  # still in flight
+    assert e.value.status == sd.SD_ERR_STATE
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[1].sd_outer_grad_quantize(1, 15, x, x, rep.slot(0), n)  # fine...
+        rep.ctx[1].sd_fragment_sync(1, 15, rep.gather, n)              # ...but slot 0 is not rank 1's
+    assert e.value.status == sd.SD_ERR_ARG
+    rep.ctx[0].sd_fragment_sync(0, 10, rep.gather, n)
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[0].sd_merge(0, 12, rep.gather, x, x, x, n)  # tau = 1: receive at 11
+    assert e.value.status == sd.SD_ERR_SCHEDULE
+    with pytest.raises(sd.SdError) as e:
+        rep.ctx[0].sd_merge(0, 11, rep.gather, x[1:], x, x, n)  # misaligned theta
+    assert e.value.status == sd.SD_ERR_ARG
+    torch.cuda.synchronize()
+    rep.close()
+
+
+# ---------------------------------------------------------------- toy, e2e
+def test_toy_config_alg2_end_to_end():
+    """BASELINE.json configs[0]: M=2, 2^20 fp32 params in 2 fragments, H=10,
+    tau=1, T=100.  Every step: synthetic inner step on each replica, then the
+    calendar's sends and receives through libsd; final theta (both
+    replicas), anchors and momenta bit-identical to or_toy_run."""
+    M, bl, H, tau, T = 2, 2 ** 19, 10, 1, 100
+    c_or = oracle.config(L=2, fs=1, H=H, tau=tau, T=T)
+    th_o, A_o, v_o, sent_o, st = oracle.toy_run(c_or, M, bl, synth.SEED)
+    assert st == 0
+    cfg = sd.sd_config_default(2, 1, H, tau=tau, T=T)
+    P = sd.sd_fragment_count(cfg)
+    n = bl
+    reps = [EmulatedReplicas(cfg, M, n) for _ in range(P)]
+    A = [[synth.dev_init(torch.empty(n, device=DEV), synth.flat_segments(n), p) for _ in range(M)] for p in range(P)]
+    v = [[torch.zeros(n, device=DEV) for _ in range(M)] for p in range(P)]
+    th = [torch.cat([A[p][0] for p in range(P)]).clone() for _ in range(M)]  # replica m's full vector
+    frag = lambda m, p: th[m][p * n:(p + 1) * n]
+    sent = 0
+    for t in range(1, T + 1):
+        for m in range(M):
+            synth.dev_apply_toy(th[m], m, t)
+        send, recv = sd.sd_fragment_schedule(cfg, t)
+        for p in send:
+            reps[p].quantize_all(p, t, [frag(m, p) for m in range(M)], A[p])
+            sent += M * reps[p].pb
+        for p in recv:
+            reps[p].merge_all(p, t, [frag(m, p) for m in range(M)], A[p], v[p])
+    torch.cuda.synchronize()
+    assert sent == sent_o
+    for m in range(M):
+        assert_same(th[m], th_o[m], f"theta replica {m}")
+    for p in range(P):
+        for m in range(M):
+            assert_same(A[p][m], A_o[p * n:(p + 1) * n], f"anchor fragment {p}")
+            assert_same(v[p][m], v_o[p * n:(p + 1) * n], f"momentum fragment {p}")
+    for r in reps:
+        r.close()
+
+
+# ------------------------------------------------- full size, bench layout
+@pytest.mark.parametrize("shape", ["1B", "4B_last"])
+def test_full_size_sampled_blocks(shape):
+    """BASELINE.json full sizes in the bench's launch configuration: the 1B
+    fragment (n = 151,007,616, M = 2) and the 4B last fragment (n =
+    438,064,512 incl. embedding, M = 4), emulated on one GPU.  The oracle
+    recomputes sampled 1024-element scale blocks one by one (each block's
+    codes, scale and outputs depend only on that block), inputs regenerated
+    on the host from the same counter-based generator."""
+    if shape == "1B":
+        d, layers, emb, M = 2048, [0, 8, 16], False, 2
+    else:
+        d, layers, emb, M = 3072, [11, 23, 35], True, 4
+    segs = synth.fragment_segments(d, layers, emb)
+    n = synth.segments_numel(segs)
+    p, r, B = 0, 1, 1024
+    cfg = cfg_for(B, tau=1)
+    rep = EmulatedReplicas(cfg, M, n)
+    A_d = synth.dev_init(torch.empty(n, device=DEV), segs, p)
+    Acopies = [A_d] + [A_d.clone() for _ in range(M - 1)]
+    v_d = [torch.zeros(n, device=DEV) for _ in range(M)]
+    th_d = []
+    for m in range(M):
+        th = A_d.clone()
+        synth.dev_apply_window(th, segs, p, m, r)
+        th_d.append(th)
+    rep.quantize_all(p, 10, th_d, Acopies)
+    for m in range(M):
+        synth.dev_apply_drift(th_d[m], segs, p, m, r)
+    rep.merge_all(p, 11, th_d, Acopies, v_d)
+    torch.cuda.synchronize()
+    nb = -(-n // B)
+    rng = np.random.default_rng(4)
+    blocks = sorted(set([0, nb - 1] + list(rng.integers(0, nb, 48))))
+    soff = sd.sd_payload_scales_offset(n)
+    gat = rep.gather
+    for b in blocks:
+        lo, hi = b * B, min(n, (b + 1) * B)
+        A0 = synth.host_init(segs, p, lo, hi)
+        sends = [synth.host_apply_window(A0.copy(), segs, p, m, r, i0=lo) for m in range(M)]
+        merges = [synth.host_apply_drift(s.copy(), segs, p, m, r, i0=lo) for m, s in enumerate(sends)]
+        Ao, vo = A0.copy(), np.zeros(hi - lo, np.float32)
+        st, g_o = oracle.round_(sends, merges, Ao, vo, B=B)
+        assert st == 0
+        pb_o = oracle.payload_bytes(hi - lo, B)
+        for m in range(M):
+            base = m * rep.pb
+            got_codes = gat[base + lo // 2: base + (hi + 1) // 2].cpu().numpy()
+            assert np.array_equal(got_codes, g_o[m * pb_o: m * pb_o + (hi - lo + 1) // 2]), f"block {b} codes"
+            got_s = gat[base + soff + 4 * b: base + soff + 4 * b + 4].cpu().numpy()
+            so = oracle.scales_offset(hi - lo)
+            assert np.array_equal(got_s, g_o[m * pb_o + so: m * pb_o + so + 4]), f"block {b} scale"
+            assert_same(Acopies[m][lo:hi], Ao, f"block {b} anchor")
+            assert_same(v_d[m][lo:hi], vo, f"block {b} momentum")
+            assert_same(th_d[m][lo:hi], merges[m], f"block {b} theta")
+    rep.close()
