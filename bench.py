@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""Benchmark of Streaming DiLoCo's per-fragment outer synchronization on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload 1B] [--impl ours|reference]
+
+One process per GPU (torchrun for N > 1), replica m = rank, M = N replicas.
+A step is one pass of the whole hot path for the
+next fragment on the calendar: schedule -> k_quantize -> NCCL all-gather ->
+block-receive -> k_apply (decode + fp32 mean + Nesterov + alpha-merge),
+cycling through all P fragments of the workload (1B: 8 fragments of
+151M-217M fp32 params, arrays > L2, so no flush is needed).  Inputs are
+resident in HBM (synthetic, seeded, synth/); `e2e` repeats the steps through
+the same C-ABI calls with the fragment's parameters coming from and going
+back to pinned host memory inside the timed region.
+
+Timing: W untimed warm-up steps, then exactly K steps between a barrier +
+cuda synchronize on both sides, CUDA events on the compute stream, max over
+ranks.  Rank 0 prints one JSON line.  `--impl reference` times the CPU
+oracle (oracle/, single thread) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+UNIT = "params/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        j = json.load(open(path))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="1B", choices=["toy", "35M", "1B", "4B"])
+    ap.add_argument("--scale-block", type=int, default=1024)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-m-sweep", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms, host-stamped."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.samples = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    self.samples.append((time.time(), float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+                except ValueError:
+                    pass
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "note": "nvidia-smi unavailable"}
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        window = "timed region"
+        if len(win) < 3:
+            win = [s for s in self.samples if s[3] > 0] or self.samples
+            window = "whole GPU phase (timed region shorter than 3 samples)"
+        reasons = sorted({self.NAMES[i] for s in win for i, v in enumerate(s[4]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": max(s[2] for s in win),
+                "reasons": reasons, "samples": len(win), "window": window}
+
+
+# --------------------------------------------------------------------------- workload
+def algorithmic_bytes(n: int, M: int, B: int):
+    """quantize reads theta, A (8 B) and writes 0.5 B of codes
+    + 4/B of scales; apply reads A, v, theta (12 B) + M payloads and writes
+    A, v, theta (12 B).  B = 0: one scale per fragment."""
+    nb = 1 if B == 0 else -(-n // B)
+    pay = n / 2 + 4 * nb
+    return 8 * n + pay, 24 * n + M * pay
+
+
+def calendar_sends(sd, cfg, count: int):
+    """The first `count` (fragment, send step) events from t = H on (libsd's scheduler)."""
+    out, t = [], cfg.H
+    while len(out) < count:
+        send, _ = sd.sd_fragment_schedule(cfg, t)
+        out.extend((p, t) for p in send)
+        t += 1
+    return out[:count]
+
+
+def make_cfg(sd, wl, B):
+    return sd.sd_config_default(wl.layers, wl.fragment_size, wl.H, tau=wl.tau, alpha=wl.alpha, outer_lr=wl.lr,
+                                outer_momentum=wl.mu, scale_block=B)
+
+
+def workload_config(wl, B, world):
+    return {"workload": wl.describe() + f"; M = {world} replica(s), one per GPU; E3M0 B={B}",
+            "fragments": None, "l2": "inputs > L2 (fragments of 0.6-0.9 GB per fp32 array, cycled); no flush",
+            "parallelism": f"diloco-replicas{world}"}
+
+
+# --------------------------------------------------------------------------- oracle timing
+def oracle_sample_rate(wl, B, M, p, segs, S, reps=1):
+    """Runs the CPU oracle's full round (or_round: quantize M replicas, mean,
+    Nesterov, merge M replicas) on the first S elements of fragment p.
+    Returns (seconds per round, elements per round)."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    A = synth.host_init(segs, p, 0, S)
+    thetas = [synth.host_apply_window(A.copy(), segs, p, m, 1) for m in range(M)]
+    merges = [t.copy() for t in thetas]
+    v = np.zeros(S, np.float32)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.round_(thetas, merges, A, v, B=B, lr=wl.lr, mu=wl.mu, alpha=wl.alpha)
+    return (time.perf_counter() - t0) / reps, S
+
+
+def cpu_baseline(wl, B, M, segs0, n0, target_s):
+    import oracle  # noqa: F401  (test infrastructure, allowed in this leg only)
+
+    S0 = min(n0, 1 << 20)
+    dt, _ = oracle_sample_rate(wl, B, M, 0, segs0, S0)
+    S = int(min(n0, max(S0, S0 * target_s / max(dt, 1e-6))))
+    S -= S % 1024 if S > 1024 else 0
+    dt, S = oracle_sample_rate(wl, B, M, 0, segs0, S)
+    return {"value": S * M / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"or_round on the first {S} elements of fragment 0 for all M={M} replicas "
+                      f"({dt:.2f} s, single thread, -O2 -ffp-contract=off)"}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    import synth
+    from synth.workloads import WORKLOADS
+    from paper_2501_18512_b200 import sd
+
+    wl = WORKLOADS[args.workload]
+    B = args.scale_block
+    cfg = make_cfg(sd, wl, B)
+    P = sd.sd_fragment_count(cfg)
+    lay = [sd.sd_fragment_layout(cfg, p) for p in range(P)]
+    segs = [wl.segments(b, e) for b, _, e in lay]
+    M = world
+    nmin = min(synth.segments_numel(s) for s in segs)
+    dt, _ = oracle_sample_rate(wl, B, M, 0, segs[0], min(1 << 18, nmin))
+    per_step = min(2.0, 90.0 / max(1, args.steps + args.warmup))
+    S = int(min(nmin, max(1 << 16, min(1 << 18, nmin) * per_step / max(dt, 1e-6))))
+    S -= S % 1024 if S > 1024 else 0
+    events = calendar_sends(sd, cfg, args.warmup + args.steps)
+    for p, _ in events[:args.warmup]:
+        oracle_sample_rate(wl, B, M, p, segs[p], S)
+    total = 0.0
+    for p, _ in events[args.warmup:]:
+        dt, _ = oracle_sample_rate(wl, B, M, p, segs[p], S)
+        total += dt
+    value = args.steps * S * M / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(wl, B, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"per step: or_round on the first {S} elements of the calendar's fragment, "
+                                   f"all M={M} replicas, single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from synth.workloads import WORKLOADS
+    from paper_2501_18512_b200 import FragmentSync, sd
+
+    rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[args.workload]
+    B = args.scale_block
+    M = world
+    cfg = make_cfg(sd, wl, B)
+    P = sd.sd_fragment_count(cfg)
+    lay = [sd.sd_fragment_layout(cfg, p) for p in range(P)]
+    segs = [wl.segments(b, e) for b, _, e in lay]
+    n = [synth.segments_numel(s) for s in segs]
+
+    # outer-state store (a2): every fragment's anchor, momentum and live params resident in HBM
+    A = [synth.dev_init(torch.empty(n[p], device=dev), segs[p], p) for p in range(P)]
+    v = [torch.zeros(n[p], device=dev) for p in range(P)]
+    theta = []
+    for p in range(P):
+        th = A[p].clone()
+        synth.dev_apply_window(th, segs[p], p, rank, 1)
+        theta.append(th)
+    sync = FragmentSync(cfg, n, rank, world, local)
+    torch.cuda.synchronize()
+
+    K, W = args.steps, args.warmup
+    events = calendar_sends(sd, cfg, W + K)
+    sampler = ClockSampler(local)
+
+    def one_step(p, t, ev=None):
+        ctx = sync.ctx
+        if ev is not None:
+            ev[0].record()
+        ctx.sd_outer_grad_quantize(p, t, theta[p], A[p], sync.slot(p), n[p])     # a1 + a3
+        if ev is not None:
+            ev[1].record()
+        ctx.sd_fragment_sync(p, t, sync.gather[p], n[p])                          # a4
+        ctx.sd_fragment_wait(p, t + cfg.tau)                                      # a5
+        if ev is not None:
+            ev[2].record()
+        ctx.sd_merge(p, t + cfg.tau, sync.gather[p], theta[p], A[p], v[p], n[p])  # a6
+        if ev is not None:
+            ev[3].record()
+
+    for p, t in events[:W]:
+        one_step(p, t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = sd.sd_kernel_launch_count()
+    torch.cuda.synchronize()
+    w0 = time.time()
+    start.record()
+    for i, (p, t) in enumerate(events[W:]):
+        one_step(p, t, kev[i])
+    stop.record()
+    torch.cuda.synchronize()
+    w1 = time.time()
+    if world > 1:
+        dist.barrier()
+    launches = sd.sd_kernel_launch_count() - launches0
+    ms = start.elapsed_time(stop)
+    q_ms = [e[0].elapsed_time(e[1]) for e in kev]
+    a_ms = [e[2].elapsed_time(e[3]) for e in kev]
+    if world > 1:
+        tms = torch.tensor([ms], device=dev)
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        ms = float(tms.item())
+    st, fb = sync.check()
+    if st != sd.SD_OK:
+        raise SystemExit(f"libsd reported {sd.STATUS_NAMES[st]} (first bad index {fb})")
+
+    elems = sum(n[p] for p, _ in events[W:])            # fragment elements per replica over K steps
+    value = elems * world / (ms / 1e3)                   # whole job: all replicas' elements / max time
+    qb = sum(algorithmic_bytes(n[p], M, B)[0] for p, _ in events[W:])
+    ab = sum(algorithmic_bytes(n[p], M, B)[1] for p, _ in events[W:])
+    q_gbs = qb / (sum(q_ms) / 1e3) / 1e9
+    a_gbs = ab / (sum(a_ms) / 1e3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath)).get(f"k_apply/{args.workload}/M{M}/B{B}")
+        if tj:
+            traffic = tj["dram_bytes_per_launch"]
+
+    # ---- end to end: the same calls, parameters from / to pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty(n[p], dtype=torch.float32, pin_memory=True) for p in range(P)]
+        for p in range(P):
+            host[p].copy_(theta[p])
+        e_events = calendar_sends(sd, cfg, W + K + W + K)[W + K:]
+
+        def e2e_step(p, t):
+            theta[p].copy_(host[p], non_blocking=True)
+            one_step(p, t)
+            host[p].copy_(theta[p], non_blocking=True)
+
+        for p, t in e_events[:W]:
+            e2e_step(p, t)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for p, t in e_events[W:]:
+            e2e_step(p, t)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tms = torch.tensor([ems], device=dev)
+            dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+            ems = float(tms.item())
+        eel = sum(n[p] for p, _ in e_events[W:])
+        e2e = {"value": eel * world / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * eel // K, "d2h_bytes_per_step": 4 * eel // K,
+               "ms_per_step": ems / K, "path": "pinned host theta -> H2D -> sd_* C-ABI calls -> D2H, per step"}
+    sampler.stop()
+    clocks = sampler.summary(w0, w1)
+
+    # ---- per-GPU kernel work at M = 1/2/4/8 replicas, emulated on this GPU (1 fragment)
+    m_sweep = None
+    if world == 1 and not args.no_m_sweep:
+        m_sweep = m_sweep_run(torch, sd, synth, cfg, segs[0], n[0], B, dev, peak)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, B, M, segs[0], n[0], args.cpu_seconds)
+
+    if rank == 0:
+        avg_a = statistics.fmean(a_ms)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
+            "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n]),
+            "per_gpu_value": value / world,
+            "roofline": {"bound": "hbm", "kernel": "k_apply", "achieved": a_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": a_gbs / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_elem": 24 + M * (0.5 + (4.0 / B if B else 0.0)),
+                         "avg_launch_ms": avg_a},
+            "kernels": {
+                "k_quantize": {"avg_ms": statistics.fmean(q_ms), "achieved_GBps": q_gbs, "frac": q_gbs / peak,
+                               "algorithmic_bytes_per_elem": 8.5 + (4.0 / B if B else 0.0)},
+                "k_apply": {"avg_ms": avg_a, "achieved_GBps": a_gbs, "frac": a_gbs / peak},
+                "critical_path_frac": (qb + ab) / ((sum(q_ms) + sum(a_ms)) / 1e3) / 1e9 / peak,
+                "step_share": {"k_quantize": sum(q_ms) / ms, "k_apply": sum(a_ms) / ms},
+            },
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "m_sweep_emulated": m_sweep,
+        }
+        print(json.dumps(line))
+    sync.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def m_sweep_run(torch, sd, synth, cfg, segs, n, B, dev, peak, iters=12):
+    """Per-GPU kernel time of one fragment round at M = 1, 2, 4, 8 replicas,
+    the M payloads produced on this GPU by M emulated replicas (include/sd.h's
+    single-GPU seam).  Times replica 0's k_quantize and k_apply."""
+    out = {}
+    A = synth.dev_init(torch.empty(n, device=dev), segs, 0)
+    v = torch.zeros(n, device=dev)
+    for M in (1, 2, 4, 8):
+        ctx = [sd.SdContext(cfg, m, M, None, dev.index) for m in range(M)]
+        pb = sd.sd_payload_bytes(cfg, n)
+        gather = torch.empty(M * pb, dtype=torch.uint8, device=dev)
+        th = []
+        for m in range(M):
+            x = A.clone()
+            synth.dev_apply_window(x, segs, 0, m, 1)
+            th.append(x)
+        qs, as_ = [], []
+        t = cfg.H
+        for it in range(iters + 2):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            for m in range(M):
+                if m == 0:
+                    e[0].record()
+                ctx[m].sd_outer_grad_quantize(0, t, th[m], A, gather[m * pb:(m + 1) * pb], n)
+                if m == 0:
+                    e[1].record()
+            for m in range(M):
+                ctx[m].sd_fragment_sync(0, t, gather, n)
+            for m in range(M):
+                if m == 0:
+                    e[2].record()
+                ctx[m].sd_merge(0, t + cfg.tau, gather, th[m], A, v, n)
+                if m == 0:
+                    e[3].record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                qs.append(e[0].elapsed_time(e[1]))
+                as_.append(e[2].elapsed_time(e[3]))
+        for c in ctx:
+            c.sd_finalize()
+        qb, ab = algorithmic_bytes(n, M, B)
+        tq, ta = statistics.median(qs), statistics.median(as_)
+        out[str(M)] = {"quantize_ms": tq, "apply_ms": ta, "apply_frac": ab / (ta / 1e3) / 1e9 / peak,
+                       "quantize_frac": qb / (tq / 1e3) / 1e9 / peak,
+                       "params_per_s_per_gpu": n / ((tq + ta) / 1e3),
+                       "critical_path_frac": (qb + ab) / ((tq + ta) / 1e3) / 1e9 / peak}
+        del gather, th
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -20,7 +20,7 @@
  *  - Every function returns sd_status; nothing throws, exits or prints.
  *    A failing call leaves a message in sd_last_error(ctx) (thread-local
  *    when ctx == NULL) naming the offending values.
- *  - Device pointers are CUDA device addresses of the ctx's device, 16-byte
+ *  - Device pointers are CUDA device addresses of the ctx's device, 32-byte
  *    aligned (256 recommended; gather buffers MUST be 256-byte aligned).
  *    The caller owns all device memory (theta, anchor, momentum, gather
  *    buffers) and must keep it alive until the stream work using it is done;
@@ -162,6 +162,12 @@ sd_status sd_outer_grad_quantize(sd_ctx* ctx, int32_t p, int64_t t, const float*
  * only orders streams. */
 sd_status sd_fragment_sync(sd_ctx* ctx, int32_t p, int64_t t, void* gather_buf, int64_t n,
                            sd_stream stream);
+
+/* Alg. 2 L11 block-receive on its own (§8(a) a5): `stream` waits for the
+ * all-gather of p, whose receive falls at t.  Optional: sd_merge performs
+ * the same wait; splitting it out lets a caller time the merge kernel
+ * apart from any exposed gather time. */
+sd_status sd_fragment_wait(sd_ctx* ctx, int32_t p, int64_t t, sd_stream stream);
 
 /* Alg. 2 L11-13 (§8(a) a5 + a6): `stream` waits for the gather of p
  * (block-receive), then one fused kernel: decode + M-way fp32 mean in

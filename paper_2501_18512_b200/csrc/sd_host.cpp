@@ -337,8 +337,8 @@ sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, floa
   if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
   if (n == 0) return SD_OK;
   sd_status st;
-  if ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")) ||
-      (st = check_ptr(c, momentum, 16, "momentum")))
+  if ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")) ||
+      (st = check_ptr(c, momentum, 32, "momentum")))
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
@@ -359,7 +359,7 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
     return ctx_fail(c, SD_ERR_STATE, "fragment %d is still in flight (sent at step %lld)", p,
                     (long long)c->fl[p].send_step);
   if ((st = check_ptr(c, slot_out, 256, "slot_out"))) return st;
-  if (n > 0 && ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")))) return st;
+  if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")))) return st;
   const sdk::Payload pl = payload_of(&c->cfg, n);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
@@ -405,6 +405,22 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
   return SD_OK;
 }
 
+sd_status sd_fragment_wait(sd_ctx* c, int32_t p, int64_t t, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, t, 0))) return st;
+  const int64_t s_step = receive_send_step(&c->cfg, p, t);
+  if (s_step == 0)
+    return ctx_fail(c, SD_ERR_SCHEDULE, "fragment %d is not scheduled to be received at step %lld (tau = %d)", p,
+                    (long long)t, c->cfg.tau);
+  if (c->fl[p].state != SYNCED || c->fl[p].send_step != s_step)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d: wait at step %lld needs the sync of step %lld first", p,
+                    (long long)t, (long long)s_step);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->done[p], 0));
+  return SD_OK;
+}
+
 sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
                    float* momentum, int64_t n, sd_stream stream) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
@@ -421,8 +437,8 @@ sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   if (f.n != n) return ctx_fail(c, SD_ERR_ARG, "fragment %d: n = %lld but synced n = %lld", p, (long long)n, (long long)f.n);
   if (f.gather != gather_buf)
     return ctx_fail(c, SD_ERR_ARG, "fragment %d: gather_buf %p is not the synced buffer %p", p, gather_buf, f.gather);
-  if (n > 0 && ((st = check_ptr(c, theta, 16, "theta")) || (st = check_ptr(c, anchor, 16, "anchor")) ||
-                (st = check_ptr(c, momentum, 16, "momentum"))))
+  if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")) ||
+                (st = check_ptr(c, momentum, 32, "momentum"))))
     return st;
   const sdk::Payload pl = payload_of(&c->cfg, n);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

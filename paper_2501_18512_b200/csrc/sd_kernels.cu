@@ -4,19 +4,27 @@
 //
 //   k_quantize  Alg. 2 L7 + E3M0
 //               Delta = A - theta, per-block absmax (warp REDUX), exact
-//               E3M0 thresholds, nibble pack, payload trailer.
+//               E3M0 code, nibble pack, payload trailer.
 //   k_apply     Alg. 2 L8 receive side + L12 + L13
 //               decode, M-way fp32 sum in ascending replica order, /M,
 //               Nesterov, anchor update, alpha-merge.
 //   k_absmax + k_encode: the two-pass variant for B = 0 (one scale per
 //               fragment) and B > 1024.
 //
-// Arithmetic: every float op is an explicit round-to-nearest intrinsic
-// (__fadd_rn/__fsub_rn/__fmul_rn/__fdiv_rn) and the file is compiled with
-// -fmad=false, so nothing is contracted into an FMA (DESIGN.md §2 AMB-15).
-// E3M0 encoding compares |Delta| against per-block fp32 thresholds T_j, each
-// the smallest binary32 x with x^2 >= s^2 2^(-2j-1) (checked in exact binary64
-// arithmetic), so the codes are exactly the nearest-in-log2 rule.
+// Memory: every lane moves 8 consecutive fp32 with one 256-bit access
+// (sm_100 LDG.256 / STG.256), so a warp instruction covers 1 KB and a lane's
+// 8 codes are one 32-bit word of the payload.
+//
+// Arithmetic: every float op is an explicit round-to-nearest intrinsic and the
+// file is compiled with -fmad=false: nothing is contracted into an FMA
+// (DESIGN.md §2 AMB-15), so the results equal the oracle's bit for bit.
+//
+// Exact E3M0: code e = #{j in 0..6 : |d| >= T_j}, T_j the
+// smallest binary32 with T_j^2 >= s^2 2^(-2j-1) (checked in exact binary64).
+// While T_6 is a normal number, T_j = T_0 / 2^j exactly, i.e. bits(T_j) =
+// bits(T_0) - j 2^23, and since |d| <= s < 2 T_0 the count is the integer
+//   e = max(0, 7 - ((bits(T_0) + 2^23 - 1 - bits(|d|)) >> 23)).
+// Blocks whose T_6 would be subnormal (s < ~2^-119.5) take the 7-compare path.
 #include <cuda_runtime.h>
 #include <float.h>
 #include <math_constants.h>
@@ -30,6 +38,39 @@ namespace {
 constexpr uint32_t kMagic = 0x31304453u;  // "SD01"
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
+constexpr uint32_t kInfBits = 0x7f800000u;
+
+struct f8 {
+  float v[8];
+};
+
+// 256-bit global accesses (sm_100): read-once streams bypass L1.
+__device__ __forceinline__ f8 ld8_stream(const float* p) {
+  f8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                 "=f"(r.v[6]), "=f"(r.v[7])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ f8 ld8(const float* p) {
+  f8 r;
+  asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                 "=f"(r.v[6]), "=f"(r.v[7])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st8(float* p, const f8& r) {
+  asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+               "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_code_word(const uint32_t* p) {
+  uint32_t w;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(w) : "l"(p));
+  return w;
+}
 
 __device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
@@ -50,33 +91,31 @@ __device__ __noinline__ float e3m0_threshold(float s, int j) {
   return c;
 }
 
-// E3M0 code of d given the block's thresholds: e = #{j : |d| >= T_j},
-// code = sign << 3 | e, and 0 (never 8) when e == 0.
-__device__ __forceinline__ uint32_t e3m0_encode(float d, const float (&T)[7]) {
+// Fast-path encode (T_0..T_6 normal): c0 = bits(T_0) + 2^23 - 1.
+__device__ __forceinline__ uint32_t encode_fast(float d, uint32_t c0) {
+  const uint32_t db = __float_as_uint(d);
+  const int k = (int)((c0 - (db & 0x7fffffffu)) >> 23);
+  const uint32_t e = (uint32_t)max(7 - k, 0);
+  return e | ((e + 7u) & (db >> 28) & 8u);  // sign bit only when e > 0 (never code 8)
+}
+
+// General encode: e = #{j : |d| >= T_j} against explicit thresholds.
+__device__ __forceinline__ uint32_t encode_slow(float d, const float (&T)[7]) {
   const float a = fabsf(d);
-  const uint32_t e = (uint32_t)(a >= T[0]) + (uint32_t)(a >= T[1]) + (uint32_t)(a >= T[2]) +
-                     (uint32_t)(a >= T[3]) + (uint32_t)(a >= T[4]) + (uint32_t)(a >= T[5]) +
-                     (uint32_t)(a >= T[6]);
-  const uint32_t sgn = (__float_as_uint(d) >> 28) & 8u;
-  return e ? (sgn | e) : 0u;
+  uint32_t e = 0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) e += (uint32_t)(a >= T[j]);
+  return e | ((e + 7u) & (__float_as_uint(d) >> 28) & 8u);
 }
 
-__device__ __forceinline__ uint32_t pack4(const float4& d, const float (&T)[7]) {
-  return e3m0_encode(d.x, T) | (e3m0_encode(d.y, T) << 4) | (e3m0_encode(d.z, T) << 8) |
-         (e3m0_encode(d.w, T) << 12);
-}
-
-__device__ __forceinline__ float4 sub4(const float4& a, const float4& b) {
-  return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
-}
-
-__device__ __forceinline__ uint32_t max_abs_bits4(const float4& d) {
-  return max(max(abs_bits(d.x), abs_bits(d.y)), max(abs_bits(d.z), abs_bits(d.w)));
+__device__ __forceinline__ bool fast_ok(float s, float t0) {
+  // all seven thresholds normal (bits(T_6) >= 2^23) and s finite, nonzero
+  return s > 0.0f && s <= FLT_MAX && __float_as_uint(t0) >= 0x03800000u;
 }
 
 struct QArgs {
-  const float4* theta;
-  const float4* anchor;
+  const float* theta;
+  const float* anchor;
   int64_t n;        // elements
   int64_t nb;       // scale blocks
   int32_t lgB;      // log2(B), or -1 for one block per fragment
@@ -84,64 +123,110 @@ struct QArgs {
   size_t scales_off, trailer_off, bytes;
 };
 
-// Loads the 8 float4 of lane `lane` in 1024-element chunk c: float4 index
-// c*256 + k*32 + lane (each warp load instruction is 512 contiguous bytes).
-// Out-of-range elements of the ragged last chunk read as 0 (Delta = +0).
+// Chunk = 1024 elements = 4 rows of 256; lane `lane` owns elements
+// c*1024 + k*256 + 8*lane .. +7 of row k (one LDG.256 per array and row).
+// Elements past n of the ragged last chunk read as Delta = +0.
 template <bool kFullChunk>
-__device__ __forceinline__ void load_chunk(const QArgs& a, int64_t c, int lane, float4 (&d)[8]) {
-  const int64_t base4 = c * 256 + lane;
+__device__ __forceinline__ void load_chunk(const QArgs& a, int64_t c, int lane, f8 (&d)[4]) {
+  const int64_t e0 = c * 1024 + 8 * lane;
   if (kFullChunk) {
-    float4 th[8], an[8];
+    f8 th[4], an[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      th[k] = __ldcs(a.theta + base4 + k * 32);
-      an[k] = __ldcs(a.anchor + base4 + k * 32);
+    for (int k = 0; k < 4; ++k) {
+      th[k] = ld8_stream(a.theta + e0 + 256 * k);
+      an[k] = ld8_stream(a.anchor + e0 + 256 * k);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = sub4(an[k], th[k]);
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[k].v[i] = __fsub_rn(an[k].v[i], th[k].v[i]);  // Alg. 2 L7
   } else {
-    const float* th = reinterpret_cast<const float*>(a.theta);
-    const float* an = reinterpret_cast<const float*>(a.anchor);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t e0 = 4 * (base4 + k * 32);
-      float v[4];
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = (e0 + i < a.n) ? __fsub_rn(an[e0 + i], th[e0 + i]) : 0.0f;
-      d[k] = make_float4(v[0], v[1], v[2], v[3]);
-    }
+      for (int i = 0; i < 8; ++i) {
+        const int64_t e = e0 + 256 * k + i;
+        d[k].v[i] = (e < a.n) ? __fsub_rn(a.anchor[e], a.theta[e]) : 0.0f;
+      }
   }
 }
 
+__device__ __forceinline__ uint32_t row_max_bits(const f8& r) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m = max(m, abs_bits(r.v[i]));
+  return m;
+}
+
 // Index of the first non-finite Delta of the chunk -> atomicMin into the trailer.
-__device__ __forceinline__ void record_first_bad(const QArgs& a, int64_t c, int lane, const float4 (&d)[8]) {
+__device__ __forceinline__ void record_first_bad(const QArgs& a, int64_t c, int lane, const f8 (&d)[4]) {
   uint32_t best = 0xffffffffu;
 #pragma unroll
-  for (int k = 7; k >= 0; --k) {
-    const uint32_t off = (uint32_t)((k * 32 + lane) * 4);
-    if (abs_bits(d[k].w) >= 0x7f800000u) best = off + 3;
-    if (abs_bits(d[k].z) >= 0x7f800000u) best = off + 2;
-    if (abs_bits(d[k].y) >= 0x7f800000u) best = off + 1;
-    if (abs_bits(d[k].x) >= 0x7f800000u) best = off;
-  }
+  for (int k = 3; k >= 0; --k)
+#pragma unroll
+    for (int i = 7; i >= 0; --i)
+      if (abs_bits(d[k].v[i]) >= kInfBits) best = (uint32_t)(256 * k + 8 * lane + i);
   best = __reduce_min_sync(kFull, best);
   if (lane == 0 && best != 0xffffffffu)
     atomicMin(reinterpret_cast<unsigned long long*>(a.slot + a.trailer_off + 8),
               (unsigned long long)(c * 1024 + best));
 }
 
-// Broadcast the 7 thresholds of block q (computed by lanes 8q..8q+6).
-__device__ __forceinline__ void gather_thresholds(float tl, int q, float (&T)[7]) {
-#pragma unroll
-  for (int j = 0; j < 7; ++j) T[j] = __shfl_sync(kFull, tl, q * 8 + j);
+// Stores one row's 8 codes (element 8*lane + i -> nibble i) as a word;
+// the ragged last chunk only writes words inside the codes region (those
+// past n hold zero codes = the zero padding up to the scales).
+__device__ __forceinline__ void store_row_codes(const QArgs& a, int64_t c, int k, int lane, uint32_t w,
+                                                bool guard) {
+  const int64_t word = (c * 1024 + 256 * k + 8 * lane) >> 3;
+  if (!guard || 4 * (size_t)word < a.scales_off) reinterpret_cast<uint32_t*>(a.slot)[word] = w;
 }
 
-template <int NB>
-__device__ __forceinline__ uint32_t select_u32(const uint32_t (&v)[NB], int q) {
-  uint32_t r = v[0];
+// Encodes the 4 rows of a chunk; s[q] = scale of block q of the chunk
+// (row k belongs to block k / (4 / NB)).
+template <int NB, bool kFullChunk>
+__device__ __forceinline__ void encode_chunk_rows(const QArgs& a, int64_t c, int lane, const f8 (&d)[4],
+                                                  const float (&s)[NB]) {
+  float sl = s[0];
 #pragma unroll
-  for (int i = 1; i < NB; ++i) r = (q == i) ? v[i] : r;
-  return r;
+  for (int q = 1; q < NB; ++q) sl = (lane == q) ? s[q] : sl;
+  const float t0_l = (lane < NB) ? e3m0_threshold(sl, 0) : 0.0f;  // T_0 of block `lane`
+  float t0[NB];
+  bool all_fast = true;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    t0[q] = __shfl_sync(kFull, t0_l, q);
+    all_fast &= fast_ok(s[q], t0[q]);
+  }
+  if (all_fast) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c0 = __float_as_uint(t0[k / (4 / NB)]) + 0x7fffffu;
+      uint32_t w = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w |= encode_fast(d[k].v[i], c0) << (4 * i);
+      store_row_codes(a, c, k, lane, w, !kFullChunk);
+    }
+  } else {  // tiny, zero or non-finite scale somewhere in the chunk: explicit thresholds
+    float tl = CUDART_INF_F;
+    {
+      const int q = lane >> 3, j = lane & 7;
+      float sq = s[0];
+#pragma unroll
+      for (int r = 1; r < NB; ++r) sq = (q == r) ? s[r] : sq;
+      if (q < NB && j < 7) tl = e3m0_threshold(sq, j);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = k / (4 / NB);
+      float T[7];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) T[j] = __shfl_sync(kFull, tl, q * 8 + j);
+      uint32_t w = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w |= encode_slow(d[k].v[i], T) << (4 * i);
+      store_row_codes(a, c, k, lane, w, !kFullChunk);
+    }
+  }
 }
 
 // Writes the payload bytes after the scales: zero pad, trailer magic + nb,
@@ -164,45 +249,28 @@ __device__ void write_tail(const QArgs& a) {
 // ---------------------------------------------------------------------------
 template <int NB, bool kFullChunk>
 __device__ __forceinline__ void quantize_chunk(const QArgs& a, int64_t c, int lane) {
-  constexpr int KB = 8 / NB;  // float4 rows per scale block
-  float4 d[8];
+  constexpr int KB = 4 / NB;  // rows per scale block
+  f8 d[4];
   load_chunk<kFullChunk>(a, c, lane, d);
-
-  uint32_t mb[NB];
+  float s[NB];
+  bool bad = false;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     uint32_t m = 0;
 #pragma unroll
-    for (int k = q * KB; k < (q + 1) * KB; ++k) m = max(m, max_abs_bits4(d[k]));
-    mb[q] = __reduce_max_sync(kFull, m);  // exact max |Delta| of the block (as bits)
+    for (int k = q * KB; k < (q + 1) * KB; ++k) m = max(m, row_max_bits(d[k]));
+    m = __reduce_max_sync(kFull, m);  // exact max |Delta| of the block (as bits)
+    bad |= m >= kInfBits;
+    s[q] = __uint_as_float(m);
   }
-  bool bad = false;
-#pragma unroll
-  for (int q = 0; q < NB; ++q) bad |= mb[q] >= 0x7f800000u;
   if (bad) record_first_bad(a, c, lane, d);
-
-  float tl = CUDART_INF_F;
-  {
-    const int q = lane >> 3, j = lane & 7;
-    if (q < NB && j < 7) tl = e3m0_threshold(__uint_as_float(select_u32<NB>(mb, q)), j);
-  }
-  uint16_t* codes = reinterpret_cast<uint16_t*>(a.slot);
-  const int64_t base4 = c * 256 + lane;
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    float T[7];
-    gather_thresholds(tl, q, T);
-#pragma unroll
-    for (int k = q * KB; k < (q + 1) * KB; ++k) {
-      const int64_t i4 = base4 + k * 32;
-      const uint16_t w = (uint16_t)pack4(d[k], T);
-      if (kFullChunk || 2 * (size_t)i4 < a.scales_off) codes[i4] = w;
-    }
-  }
+  encode_chunk_rows<NB, kFullChunk>(a, c, lane, d, s);
   if (lane < NB) {
     const int64_t blk = c * NB + lane;
-    if (blk < a.nb)
-      reinterpret_cast<float*>(a.slot + a.scales_off)[blk] = __uint_as_float(select_u32<NB>(mb, lane));
+    float sv = s[0];
+#pragma unroll
+    for (int q = 1; q < NB; ++q) sv = (lane == q) ? s[q] : sv;
+    if (blk < a.nb) reinterpret_cast<float*>(a.slot + a.scales_off)[blk] = sv;
   }
 }
 
@@ -227,19 +295,17 @@ __device__ __forceinline__ int64_t block_of_chunk(const QArgs& a, int64_t c) {
 }
 
 template <bool kFullChunk>
-__device__ __forceinline__ void absmax_chunk(const QArgs& a, int64_t c, int lane, int64_t& cur,
-                                             uint32_t& run) {
-  float4 d[8];
+__device__ __forceinline__ void absmax_chunk(const QArgs& a, int64_t c, int lane, int64_t& cur, uint32_t& run) {
+  f8 d[4];
   load_chunk<kFullChunk>(a, c, lane, d);
   uint32_t m = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) m = max(m, max_abs_bits4(d[k]));
+  for (int k = 0; k < 4; ++k) m = max(m, row_max_bits(d[k]));
   m = __reduce_max_sync(kFull, m);
-  if (m >= 0x7f800000u) record_first_bad(a, c, lane, d);
+  if (m >= kInfBits) record_first_bad(a, c, lane, d);
   const int64_t blk = block_of_chunk(a, c);
   if (blk != cur) {
-    if (cur >= 0 && lane == 0)
-      atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + cur, run);
+    if (cur >= 0 && lane == 0) atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + cur, run);
     cur = blk;
     run = 0;
   }
@@ -260,20 +326,10 @@ __global__ void __launch_bounds__(kThreads) k_absmax(QArgs a) {
 
 template <bool kFullChunk>
 __device__ __forceinline__ void encode_chunk(const QArgs& a, int64_t c, int lane) {
-  float4 d[8];
+  f8 d[4];
   load_chunk<kFullChunk>(a, c, lane, d);
-  const float s = reinterpret_cast<const float*>(a.slot + a.scales_off)[block_of_chunk(a, c)];
-  const float tl = (lane < 7) ? e3m0_threshold(s, lane) : CUDART_INF_F;
-  float T[7];
-  gather_thresholds(tl, 0, T);
-  uint16_t* codes = reinterpret_cast<uint16_t*>(a.slot);
-  const int64_t base4 = c * 256 + lane;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int64_t i4 = base4 + k * 32;
-    const uint16_t w = (uint16_t)pack4(d[k], T);
-    if (kFullChunk || 2 * (size_t)i4 < a.scales_off) codes[i4] = w;
-  }
+  const float s[1] = {reinterpret_cast<const float*>(a.slot + a.scales_off)[block_of_chunk(a, c)]};
+  encode_chunk_rows<1, kFullChunk>(a, c, lane, d, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_encode(QArgs a) {
@@ -287,9 +343,8 @@ __global__ void __launch_bounds__(kThreads) k_encode(QArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_apply: fused receive side.  Thread i handles float4 i (elements 4i..4i+3)
-// of A, v, theta (512 contiguous bytes per warp instruction) and the u16 of
-// codes 2i..2i+1 of every slot; kUnroll float4 per thread in flight.
+// k_apply: fused receive side.  Thread i owns elements 8i..8i+7: one LDG.256
+// of A, v, theta each, one 32-bit code word and one scale per slot.
 // ---------------------------------------------------------------------------
 struct AArgs {
   const uint8_t* gather;
@@ -298,31 +353,48 @@ struct AArgs {
   int64_t n;
   int32_t lgB;           // log2(B) or -1
   size_t scales_off, trailer_off;
-  float4* A;
-  float4* v;
-  float4* theta;
+  float* A;
+  float* v;
+  float* theta;
   float lr, mu, alpha, beta, invM;
   int pow2M;
   unsigned long long* status;
 };
 
-// code -> 2^(e-7) * sign, then * s in binary32 (exact unless it underflows,
-// where it rounds like the oracle's LUT[c] * s).  Codes 0 and 8 -> +0.
-__device__ __forceinline__ float e3m0_decode(uint32_t c, float s) {
-  const uint32_t e = c & 7u;
-  const uint32_t bits = e ? (((c & 8u) << 28) | ((e + 120u) << 23)) : 0u;
-  return __fmul_rn(__uint_as_float(bits), s);
+// Decodes 8 codes (nibble i = element i) into LUT values +-2^(e-7) (codes 0
+// and 8 -> +0) times s.  The LUT value's top 16 bits are the
+// bf16 pattern sign<<15 | (e+120)<<7: byte tables via PRMT build two bf16
+// per 32-bit word, the valid signs are PRMT-moved to bits 15/31, and each
+// bf16 widens to fp32 by a shift or a mask.  q = LUT * s rounds like the
+// oracle's LUT[c] * s (exact unless it underflows).
+__device__ __forceinline__ void decode8(uint32_t w, float s, float (&q)[8]) {
+  const uint32_t ctrl = w & 0x77777777u;                                  // e of each nibble
+  const uint32_t sg = w & ((ctrl + 0x77777777u) & 0x88888888u);           // sign bits of codes with e > 0
+  const uint32_t z = sg << 4;
+  const uint32_t hi_a = __byte_perm(0x3D3D3C00u, 0x3F3F3E3Eu, ctrl);       // (e+120)>>1, e = 0 -> 0
+  const uint32_t lo_a = __byte_perm(0x80008000u, 0x80008000u, ctrl);       // ((e+120)&1)<<7, e = 0 -> 0
+  const uint32_t hi_b = __byte_perm(0x3D3D3C00u, 0x3F3F3E3Eu, ctrl >> 16);
+  const uint32_t lo_b = __byte_perm(0x80008000u, 0x80008000u, ctrl >> 16);
+  uint32_t pr[4];
+  pr[0] = __byte_perm(lo_a, hi_a, 0x5140) | (__byte_perm(z, sg, 0x4400) & 0x80008000u);
+  pr[1] = __byte_perm(lo_a, hi_a, 0x7362) | (__byte_perm(z, sg, 0x5511) & 0x80008000u);
+  pr[2] = __byte_perm(lo_b, hi_b, 0x5140) | (__byte_perm(z, sg, 0x6622) & 0x80008000u);
+  pr[3] = __byte_perm(lo_b, hi_b, 0x7362) | (__byte_perm(z, sg, 0x7733) & 0x80008000u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    q[2 * k] = __fmul_rn(__uint_as_float(pr[k] << 16), s);
+    q[2 * k + 1] = __fmul_rn(__uint_as_float(pr[k] & 0xffff0000u), s);
+  }
 }
 
-__device__ __forceinline__ float apply_one(float S, float& a, float& w, float t, const AArgs& p, float& tout) {
+__device__ __forceinline__ void outer_step(float S, float& a, float& w, float& t, const AArgs& p) {
   const float g = p.pow2M ? __fmul_rn(S, p.invM) : __fdiv_rn(S, (float)p.M);     // (1/M) sum
   w = __fadd_rn(__fmul_rn(p.mu, w), g);                                            // v = mu v + g
   a = __fsub_rn(a, __fmul_rn(p.lr, __fadd_rn(g, __fmul_rn(p.mu, w))));            // A -= lr (g + mu v)
-  tout = __fadd_rn(__fmul_rn(p.alpha, t), __fmul_rn(p.beta, a));                   // alpha merge
-  return g;
+  t = __fadd_rn(__fmul_rn(p.alpha, t), __fmul_rn(p.beta, a));                      // alpha merge
 }
 
-template <int kM, int kUnroll>
+template <int kM>
 __global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
   __shared__ int skip;
   const int M = kM > 0 ? kM : p.M;
@@ -345,71 +417,47 @@ __global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
   __syncthreads();
   if (skip) return;
 
-  const int64_t n4 = p.n >> 2;
+  const int64_t n8 = p.n >> 3;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += kUnroll * nthr) {
-    float4 a[kUnroll], w[kUnroll], t[kUnroll], S[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = i0 + u * nthr;
-      if (i < n4) {
-        a[u] = p.A[i];
-        w[u] = p.v[i];
-        t[u] = __ldcs(p.theta + i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = i0 + u * nthr;
-      if (i < n4) {
-        const int64_t blk = p.lgB < 0 ? 0 : ((i << 2) >> p.lgB);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += nthr) {
+    f8 a = ld8(p.A + 8 * i);
+    f8 w = ld8(p.v + 8 * i);
+    f8 t = ld8_stream(p.theta + 8 * i);
+    const int64_t blk = p.lgB < 0 ? 0 : ((8 * i) >> p.lgB);
+    float S[8];
 #pragma unroll 8
-        for (int m = 0; m < M; ++m) {
-          const uint8_t* slot = p.gather + (size_t)m * p.pb;
-          const uint32_t c = __ldg(reinterpret_cast<const uint16_t*>(slot) + i);
-          const float s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
-          const float4 q = make_float4(e3m0_decode(c & 15u, s), e3m0_decode((c >> 4) & 15u, s),
-                                       e3m0_decode((c >> 8) & 15u, s), e3m0_decode(c >> 12, s));
-          if (m == 0) S[u] = q;
-          else S[u] = make_float4(__fadd_rn(S[u].x, q.x), __fadd_rn(S[u].y, q.y),
-                                  __fadd_rn(S[u].z, q.z), __fadd_rn(S[u].w, q.w));
-        }
-      }
+    for (int m = 0; m < M; ++m) {
+      const uint8_t* slot = p.gather + (size_t)m * p.pb;
+      const uint32_t code = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
+      const float s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
+      float q[8];
+      decode8(code, s, q);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) S[j] = (m == 0) ? q[j] : __fadd_rn(S[j], q[j]);  // ascending m
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = i0 + u * nthr;
-      if (i < n4) {
-        float4 to;
-        apply_one(S[u].x, a[u].x, w[u].x, t[u].x, p, to.x);
-        apply_one(S[u].y, a[u].y, w[u].y, t[u].y, p, to.y);
-        apply_one(S[u].z, a[u].z, w[u].z, t[u].z, p, to.z);
-        apply_one(S[u].w, a[u].w, w[u].w, t[u].w, p, to.w);
-        p.A[i] = a[u];
-        p.v[i] = w[u];
-        __stcs(p.theta + i, to);
-      }
-    }
+    for (int j = 0; j < 8; ++j) outer_step(S[j], a.v[j], w.v[j], t.v[j], p);
+    st8(p.A + 8 * i, a);
+    st8(p.v + 8 * i, w);
+    st8(p.theta + 8 * i, t);
   }
-  // ragged tail: the last n % 4 elements, one thread each
-  if (blockIdx.x == 0 && threadIdx.x < (p.n & 3)) {
-    const int64_t e = (n4 << 2) + threadIdx.x;
-    float* A = reinterpret_cast<float*>(p.A);
-    float* v = reinterpret_cast<float*>(p.v);
-    float* th = reinterpret_cast<float*>(p.theta);
+  // ragged tail: the last n % 8 elements, one thread each
+  if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
+    const int64_t e = (n8 << 3) + threadIdx.x;
     const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
     float S = 0.0f;
     for (int m = 0; m < M; ++m) {
       const uint8_t* slot = p.gather + (size_t)m * p.pb;
       const uint32_t c = (slot[e >> 1] >> ((e & 1) * 4)) & 15u;
-      const float q = e3m0_decode(c, reinterpret_cast<const float*>(slot + p.scales_off)[blk]);
-      S = (m == 0) ? q : __fadd_rn(S, q);
+      float q[8];
+      decode8(c, reinterpret_cast<const float*>(slot + p.scales_off)[blk], q);
+      S = (m == 0) ? q[0] : __fadd_rn(S, q[0]);
     }
-    float a = A[e], w = v[e], to;
-    apply_one(S, a, w, th[e], p, to);
-    A[e] = a;
-    v[e] = w;
-    th[e] = to;
+    float a = p.A[e], w = p.v[e], t = p.theta[e];
+    outer_step(S, a, w, t, p);
+    p.A[e] = a;
+    p.v[e] = w;
+    p.theta[e] = t;
   }
 }
 
@@ -429,7 +477,11 @@ int occupancy(const void* kernel) {
     if (keys[i] == kernel) return vals[i];
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
-  if (used < 32) { keys[used] = kernel; vals[used] = occ; ++used; }
+  if (used < 32) {
+    keys[used] = kernel;
+    vals[used] = occ;
+    ++used;
+  }
   return occ;
 }
 
@@ -444,11 +496,11 @@ int grid_for(K kernel, int num_sms, int64_t work_items, int items_per_block) {
 
 }  // namespace
 
-int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot,
-                    int num_sms, cudaStream_t st) {
+int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, int num_sms,
+                    cudaStream_t st) {
   QArgs a;
-  a.theta = reinterpret_cast<const float4*>(theta);
-  a.anchor = reinterpret_cast<const float4*>(anchor);
+  a.theta = theta;
+  a.anchor = anchor;
   a.n = pl.n;
   a.nb = pl.nb;
   a.lgB = ilog2_or_neg(pl.B);
@@ -473,9 +525,8 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
   return cudaGetLastError() == cudaSuccess ? launched : -1;
 }
 
-int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor,
-                 float* momentum, float lr, float mu, float alpha, unsigned long long* status,
-                 int num_sms, cudaStream_t st) {
+int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor, float* momentum,
+                 float lr, float mu, float alpha, unsigned long long* status, int num_sms, cudaStream_t st) {
   AArgs p;
   p.gather = gather;
   p.pb = pl.bytes;
@@ -484,9 +535,9 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.lgB = ilog2_or_neg(pl.B);
   p.scales_off = pl.scales_off;
   p.trailer_off = pl.trailer_off;
-  p.A = reinterpret_cast<float4*>(anchor);
-  p.v = reinterpret_cast<float4*>(momentum);
-  p.theta = reinterpret_cast<float4*>(theta);
+  p.A = anchor;
+  p.v = momentum;
+  p.theta = theta;
   p.lr = lr;
   p.mu = mu;
   p.alpha = alpha;
@@ -494,14 +545,13 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.pow2M = (M & (M - 1)) == 0;
   p.invM = 1.0f / (float)M;  // exact when M is a power of two
   p.status = status;
-  constexpr int U = 2;
-  const int64_t items = (pl.n >> 2) > 0 ? (pl.n >> 2) : 1;
+  const int64_t items = (pl.n >> 3) > 0 ? (pl.n >> 3) : 1;
   switch (M) {
-    case 1: k_apply<1, U><<<grid_for(k_apply<1, U>, num_sms, items, kThreads * U), kThreads, 0, st>>>(p); break;
-    case 2: k_apply<2, U><<<grid_for(k_apply<2, U>, num_sms, items, kThreads * U), kThreads, 0, st>>>(p); break;
-    case 4: k_apply<4, U><<<grid_for(k_apply<4, U>, num_sms, items, kThreads * U), kThreads, 0, st>>>(p); break;
-    case 8: k_apply<8, U><<<grid_for(k_apply<8, U>, num_sms, items, kThreads * U), kThreads, 0, st>>>(p); break;
-    default: k_apply<0, U><<<grid_for(k_apply<0, U>, num_sms, items, kThreads * U), kThreads, 0, st>>>(p); break;
+    case 1: k_apply<1><<<grid_for(k_apply<1>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
+    case 2: k_apply<2><<<grid_for(k_apply<2>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
+    case 4: k_apply<4><<<grid_for(k_apply<4>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
+    case 8: k_apply<8><<<grid_for(k_apply<8>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
+    default: k_apply<0><<<grid_for(k_apply<0>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
   }
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

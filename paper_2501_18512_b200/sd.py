@@ -27,7 +27,7 @@ EXPORTS = (
     "sd_config_default", "sd_config_validate", "sd_fragment_count", "sd_fragment_layout",
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_outer_state_init",
-    "sd_outer_grad_quantize", "sd_fragment_sync", "sd_merge", "sd_check", "sd_last_error",
+    "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
 
@@ -76,6 +76,7 @@ def lib():
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
             "sd_outer_grad_quantize": ([P, I32, I64, P, P, I64, P, P], I32),
             "sd_fragment_sync": ([P, I32, I64, P, I64, P], I32),
+            "sd_fragment_wait": ([P, I32, I64, P], I32),
             "sd_merge": ([P, I32, I64, P, P, P, P, I64, P], I32),
             "sd_check": ([P, pI64], I32),
             "sd_last_error": ([P], ctypes.c_char_p),
@@ -211,6 +212,9 @@ class SdContext:
 
     def sd_fragment_sync(self, p, t, gather_buf, n, stream=None):
         self._c(lib().sd_fragment_sync(self.h, p, t, _ptr(gather_buf), n, _stream(stream)))
+
+    def sd_fragment_wait(self, p, t, stream=None):
+        self._c(lib().sd_fragment_wait(self.h, p, t, _stream(stream)))
 
     def sd_merge(self, p, t, gather_buf, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n
