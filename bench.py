@@ -360,6 +360,12 @@ def main():
     sampler.stop()
     clocks = sampler.summary(w0, w1)
 
+    # ---- gather hidden behind tau synthetic inner steps? (N > 1 only)
+    overlap = None
+    if world > 1:
+        more = calendar_sends(sd, cfg, 3 * (W + K) + 12)[2 * (W + K):]
+        overlap = overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, more, dev)
+
     # ---- per-GPU kernel work at M = 1/2/4/8 replicas, emulated on this GPU (1 fragment)
     m_sweep = None
     if world == 1 and not args.no_m_sweep:
@@ -393,12 +399,81 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "m_sweep_emulated": m_sweep,
+            "overlap": overlap,
         }
         print(json.dumps(line))
     sync.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=4):
+    """SURVEY.md §8(d) hidden-gather check on the real NCCL path: per round,
+    quantize -> all-gather on the comm stream while the compute stream runs
+    tau AdamW-shaped synthetic inner steps over the whole replica (24 B/param)
+    -> block-receive -> apply.  exposed = window with the gather in flight -
+    the same tau inner steps alone; hidden <=> exposed <= 5% of the gather
+    measured alone.  All times: CUDA events on the compute stream, max over
+    ranks."""
+    import statistics as st
+
+    m1 = [torch.zeros_like(x) for x in theta]
+    m2 = [torch.zeros_like(x) for x in theta]
+    tau = cfg.tau
+    Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    step = [1]
+
+    def inner():
+        for p in range(P):
+            synth.dev_inner_adamw(theta[p], m1[p], m2[p], rank, step[0])
+        step[0] += 1
+
+    def maxr(x):
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    it = iter(events)
+    alone, gath, over, bytes_in = [], [], [], []
+    for r in range(reps + 1):
+        e = [Ev() for _ in range(6)]
+        e[0].record()
+        for _ in range(tau):
+            inner()
+        e[1].record()
+        p, t = next(it)
+        sync.ctx.sd_outer_grad_quantize(p, t, theta[p], A[p], sync.slot(p), n[p])
+        e[2].record()
+        sync.ctx.sd_fragment_sync(p, t, sync.gather[p], n[p])
+        sync.ctx.sd_fragment_wait(p, t + cfg.tau)
+        e[3].record()
+        sync.ctx.sd_merge(p, t + cfg.tau, sync.gather[p], theta[p], A[p], v[p], n[p])
+        p, t = next(it)
+        sync.ctx.sd_outer_grad_quantize(p, t, theta[p], A[p], sync.slot(p), n[p])
+        sync.ctx.sd_fragment_sync(p, t, sync.gather[p], n[p])
+        e[4].record()
+        for _ in range(tau):
+            inner()
+        sync.ctx.sd_fragment_wait(p, t + cfg.tau)
+        e[5].record()
+        sync.ctx.sd_merge(p, t + cfg.tau, sync.gather[p], theta[p], A[p], v[p], n[p])
+        torch.cuda.synchronize()
+        dist.barrier()
+        if r == 0:
+            continue
+        alone.append(maxr(e[0].elapsed_time(e[1])))
+        gath.append(maxr(e[2].elapsed_time(e[3])))
+        over.append(maxr(e[4].elapsed_time(e[5])))
+        bytes_in.append((world - 1) * sync.payload[p])
+    ta, tg, to = st.median(alone), st.median(gath), st.median(over)
+    exposed = max(0.0, to - ta)
+    gbps = st.median(bytes_in) / (tg / 1e3) / 1e9
+    return {"tau": tau, "inner_step": "AdamW-shaped synthetic pass over the whole replica, 24 B/param (synth/)",
+            "inner_window_ms": ta, "overlap_window_ms": to, "gather_alone_ms": tg, "exposed_ms": exposed,
+            "hidden": exposed <= 0.05 * tg, "inner_slowdown": to / ta if ta > 0 else None,
+            "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,
+                       "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0}}
 
 
 def m_sweep_run(torch, sd, synth, cfg, segs, n, B, dev, peak, iters=12):

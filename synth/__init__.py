@@ -150,6 +150,8 @@ def _lib_cuda():
         lib.synth_cuda_apply_window.argtypes = [P, P, ctypes.c_int, U64, I32, I32, I32, I64, I64, P]
         lib.synth_cuda_apply_drift.argtypes = [P, P, ctypes.c_int, U64, I32, I32, I32, I64, I64, P]
         lib.synth_cuda_apply_toy.argtypes = [P, U64, I32, I64, I64, I64, P]
+        lib.synth_cuda_inner_adamw.argtypes = [P, P, P, I64, U64, I32, I64, P]
+        lib.synth_cuda_inner_adamw.restype = ctypes.c_int
         for f in ("synth_cuda_fill_init", "synth_cuda_apply_window", "synth_cuda_apply_drift", "synth_cuda_apply_toy"):
             getattr(lib, f).restype = ctypes.c_int
         _cuda = lib
@@ -187,3 +189,9 @@ def dev_apply_drift(x, segs, p, m, r, i0=0, seed=SEED, stream=None):
 def dev_apply_toy(x, m, t, i0=0, seed=SEED, stream=None):
     _chk(_lib_cuda().synth_cuda_apply_toy(x.data_ptr(), seed, m, t, i0, i0 + x.numel(), _stream(stream)))
     return x
+
+
+def dev_inner_adamw(theta, m1, m2, m, t, seed=SEED, stream=None):
+    """AdamW-shaped synthetic inner step over theta (harness overlap load)."""
+    _chk(_lib_cuda().synth_cuda_inner_adamw(theta.data_ptr(), m1.data_ptr(), m2.data_ptr(), theta.numel(), seed, m, t,
+                                             _stream(stream)))

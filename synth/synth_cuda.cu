@@ -27,6 +27,23 @@ __global__ void k_synth_toy(float* __restrict__ x, uint64_t seed, int32_t m, int
     x[i - i0] = __fsub_rn(x[i - i0], syn_toy_value(seed, m, t, i));
 }
 
+// AdamW-shaped synthetic inner step (the overlap load of bench.py; a stand-in
+// for Alg. 2 L3-5, not the method): gradient from a counter
+// hash, m/v moments, bias-corrected update.  Reads theta, m, v and writes them
+// back: 24 B per parameter, like a fused optimizer pass.
+__global__ void k_inner_adamw(float* __restrict__ th, float* __restrict__ m1, float* __restrict__ m2,
+                              int64_t n, uint64_t key, float lr, float bc1, float bc2) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float g = 1e-3f * syn_U(key, (uint64_t)i);
+    const float a = 0.9f * m1[i] + 0.1f * g;
+    const float b = 0.99f * m2[i] + 0.01f * g * g;
+    m1[i] = a;
+    m2[i] = b;
+    th[i] -= lr * ((a / bc1) / (sqrtf(b / bc2) + 1e-8f));
+  }
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -67,6 +84,15 @@ int synth_cuda_apply_toy(float* x, uint64_t seed, int32_t m, int64_t t, int64_t 
                          cudaStream_t st) {
   if (i1 <= i0) return 0;
   k_synth_toy<<<grid_for(i1 - i0), 256, 0, st>>>(x, seed, m, t, i0, i1);
+  return (int)cudaGetLastError();
+}
+
+int synth_cuda_inner_adamw(float* th, float* m1, float* m2, int64_t n, uint64_t seed, int32_t m, int64_t t,
+                           cudaStream_t st) {
+  if (n <= 0) return 0;
+  const float bc1 = 1.0f - powf(0.9f, (float)t), bc2 = 1.0f - powf(0.99f, (float)t);
+  k_inner_adamw<<<148 * 8, 256, 0, st>>>(th, m1, m2, n, syn_key(seed, 9, 0, (uint64_t)m, (uint64_t)t), 1e-4f,
+                                         bc1, bc2);
   return (int)cudaGetLastError();
 }
 

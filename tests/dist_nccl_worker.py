@@ -1,0 +1,88 @@
+"""Worker for tests/test_gpu_multi.py (run under torchrun, one rank per GPU).
+
+Each rank is one replica: libsd context with an NCCL communicator (unique id
+broadcast through torch.distributed), real in-place all-gather over NVLink.
+R rounds of one fragment; after every round rank 0 collects every rank's
+gather buffer, anchor, momentum and live parameters and checks them against
+the CPU oracle (inputs regenerated on the host from the same seeded
+generator): byte-identical payloads, bit-identical outer state on every
+rank (SURVEY.md §4 "distributed tests").  Prints OK on success."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+from paper_2501_18512_b200 import FragmentSync, sd  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    B = int(os.environ.get("SD_TEST_B", "1024"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    segs = synth.fragment_segments(96, [0, 4], with_embed=True, vocab=333)
+    n = synth.segments_numel(segs)
+    cfg = sd.sd_config_default(8, 2, 40, tau=3, scale_block=B)  # P = 4 fragments, H = 40
+    P = sd.sd_fragment_count(cfg)
+    p = 2
+    _, t_p, _ = sd.sd_fragment_layout(cfg, p)
+    fsync = FragmentSync(cfg, [n] * P, rank, world, local)
+    A = synth.dev_init(torch.empty(n, device=dev), segs, p)
+    v = torch.zeros(n, device=dev)
+    th = A.clone()
+    ok = True
+    if rank == 0:
+        import oracle
+
+        A_o = synth.host_init(segs, p)
+        v_o = np.zeros(n, np.float32)
+        th_o = [A_o.copy() for _ in range(world)]
+    for r in range(1, 4):
+        t = r * cfg.H + t_p
+        assert p in sd.sd_fragment_schedule(cfg, t)[0]
+        synth.dev_apply_window(th, segs, p, rank, r)
+        fsync.send(p, t, th, A)
+        synth.dev_apply_drift(th, segs, p, rank, r)      # tau overlapped inner steps
+        assert p in sd.sd_fragment_schedule(cfg, t + cfg.tau)[1]
+        fsync.receive(p, t + cfg.tau, th, A, v)
+        torch.cuda.synchronize()
+        got = {}
+        for name, x in (("gather", fsync.gather[p]), ("A", A), ("v", v), ("theta", th)):
+            parts = [torch.empty_like(x) for _ in range(world)]
+            dist.all_gather(parts, x)
+            got[name] = [q.cpu().numpy() for q in parts]
+        if rank == 0:
+            sends = []
+            for m in range(world):
+                synth.host_apply_window(th_o[m], segs, p, m, r)
+                sends.append(th_o[m].copy())
+                synth.host_apply_drift(th_o[m], segs, p, m, r)
+            st, g_o = oracle.round_(sends, th_o, A_o, v_o, B=B)
+            assert st == 0
+            for m in range(world):
+                ok &= np.array_equal(got["gather"][m], g_o)
+                ok &= np.array_equal(got["A"][m].view(np.uint32), A_o.view(np.uint32))
+                ok &= np.array_equal(got["v"][m].view(np.uint32), v_o.view(np.uint32))
+                ok &= np.array_equal(got["theta"][m].view(np.uint32), th_o[m].view(np.uint32))
+            print(f"round {r}: {'match' if ok else 'MISMATCH'}", flush=True)
+    st, fb = fsync.check()
+    ok &= st == sd.SD_OK
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    fsync.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("OK" if flag.item() == 1 else "FAIL", flush=True)
+    return 0 if flag.item() == 1 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
