@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-m-sweep", action="store_true")
+    ap.add_argument("--serial", action="store_true", help="no send/receive pipelining across fragments")
     return ap.parse_args()
 
 
@@ -261,11 +262,12 @@ def main():
     sync = FragmentSync(cfg, n, rank, world, local)
     torch.cuda.synchronize()
 
-    K, W = args.steps, args.warmup
+    K, W = args.steps, max(1, args.warmup)
     events = calendar_sends(sd, cfg, W + K)
     sampler = ClockSampler(local)
 
     def one_step(p, t, ev=None):
+        """Serialized round of fragment p: quantize, gather, block-receive, apply."""
         ctx = sync.ctx
         if ev is not None:
             ev[0].record()
@@ -280,40 +282,89 @@ def main():
         if ev is not None:
             ev[3].record()
 
-    for p, t in events[:W]:
-        one_step(p, t)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = sd.sd_kernel_launch_count()
-    torch.cuda.synchronize()
-    w0 = time.time()
-    start.record()
-    for i, (p, t) in enumerate(events[W:]):
-        one_step(p, t, kev[i])
-    stop.record()
-    torch.cuda.synchronize()
-    w1 = time.time()
-    if world > 1:
-        dist.barrier()
-    launches = sd.sd_kernel_launch_count() - launches0
-    ms = start.elapsed_time(stop)
+    pending = []
+
+    def pipe_step(p, t, ev=None):
+        """Send of fragment p (quantize + async gather), then the receive of the
+        fragment sent one step earlier: its gather ran concurrently with this
+        quantize (tau >= 1: the receive comes after later compute)."""
+        ctx = sync.ctx
+        if ev is not None:
+            ev[0].record()
+        ctx.sd_outer_grad_quantize(p, t, theta[p], A[p], sync.slot(p), n[p])
+        if ev is not None:
+            ev[1].record()
+        ctx.sd_fragment_sync(p, t, sync.gather[p], n[p])
+        if pending:
+            pp, tt = pending.pop()
+            ctx.sd_fragment_wait(pp, tt + cfg.tau)
+            if ev is not None:
+                ev[2].record()
+            ctx.sd_merge(pp, tt + cfg.tau, sync.gather[pp], theta[pp], A[pp], v[pp], n[pp])
+            if ev is not None:
+                ev[3].record()
+        elif ev is not None:
+            ev[2].record()
+            ev[3].record()
+        pending.append((p, t))
+
+    def drain():
+        while pending:
+            pp, tt = pending.pop()
+            sync.ctx.sd_fragment_wait(pp, tt + cfg.tau)
+            sync.ctx.sd_merge(pp, tt + cfg.tau, sync.gather[pp], theta[pp], A[pp], v[pp], n[pp])
+
+    pipelined = P > 1 and not args.serial
+    step_fn = pipe_step if pipelined else one_step
+
+    def timed(evs, fn):
+        for p, t in evs[:W]:
+            fn(p, t)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        kev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = sd.sd_kernel_launch_count()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        start.record()
+        for i, (p, t) in enumerate(evs[W:]):
+            fn(p, t, kev[i])
+        stop.record()
+        torch.cuda.synchronize()
+        t1 = time.time()
+        nl = sd.sd_kernel_launch_count() - l0
+        drain()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return start.elapsed_time(stop), kev, nl, t0, t1
+
+    ms, kev, launches, w0, w1 = timed(events, step_fn)
+    launches0 = 0
     q_ms = [e[0].elapsed_time(e[1]) for e in kev]
     a_ms = [e[2].elapsed_time(e[3]) for e in kev]
     if world > 1:
         tms = torch.tensor([ms], device=dev)
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         ms = float(tms.item())
+    ms_serial = None
+    if pipelined and world > 1:
+        ser_events = calendar_sends(sd, cfg, 4 * (W + K) + 12)[3 * (W + K) + 12:]
+        ms_serial, _, _, _, _ = timed(ser_events, one_step)
+        tms = torch.tensor([ms_serial], device=dev)
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        ms_serial = float(tms.item())
     st, fb = sync.check()
     if st != sd.SD_OK:
         raise SystemExit(f"libsd reported {sd.STATUS_NAMES[st]} (first bad index {fb})")
 
-    elems = sum(n[p] for p, _ in events[W:])            # fragment elements per replica over K steps
+    applied = events[W - 1:W + K - 1] if pipelined else events[W:]
+    elems = sum(n[p] for p, _ in applied)                # fragment elements per replica over K steps
     value = elems * world / (ms / 1e3)                   # whole job: all replicas' elements / max time
     qb = sum(algorithmic_bytes(n[p], M, B)[0] for p, _ in events[W:])
-    ab = sum(algorithmic_bytes(n[p], M, B)[1] for p, _ in events[W:])
+    ab = sum(algorithmic_bytes(n[p], M, B)[1] for p, _ in applied)
     q_gbs = qb / (sum(q_ms) / 1e3) / 1e9
     a_gbs = ab / (sum(a_ms) / 1e3) / 1e9
     peak, peak_src = peaks()
@@ -383,6 +434,10 @@ def main():
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
             "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n]),
             "per_gpu_value": value / world,
+            "schedule": ("pipelined: each step sends fragment k (quantize + async NCCL all-gather) and receives "
+                         "fragment k-1 (block-receive + apply), so a gather overlaps the next step's kernels "
+                         "(tau >= 1)" if pipelined else "serialized: quantize, gather, block-receive, apply per step"),
+            "value_serialized": (elems * world / (ms_serial / 1e3)) if ms_serial else None,
             "roofline": {"bound": "hbm", "kernel": "k_apply", "achieved": a_gbs, "peak": peak, "unit": "GB/s",
                          "frac": a_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_elem": 24 + M * (0.5 + (4.0 / B if B else 0.0)),

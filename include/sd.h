@@ -22,10 +22,13 @@
  *    when ctx == NULL) naming the offending values.
  *  - Device pointers are CUDA device addresses of the ctx's device, 32-byte
  *    aligned (256 recommended; gather buffers MUST be 256-byte aligned).
- *    The caller owns all device memory (theta, anchor, momentum, gather
- *    buffers) and must keep it alive until the stream work using it is done;
- *    the library allocates no device memory of its own (NCCL internals
- *    apart) and writes only slot_out, gather_buf, anchor, momentum, theta.
+ *    The caller owns theta, anchor and momentum and must keep them alive
+ *    until the stream work using them is done.  Gather buffers are either
+ *    caller-owned device memory or (recommended) allocated by
+ *    sd_gather_alloc in NCCL symmetric memory, which lets the all-gather run
+ *    on the copy engines with zero SMs.  Apart from those and NCCL
+ *    internals the library allocates no device memory, and it writes only
+ *    slot_out, gather_buf, anchor, momentum and theta.
  *  - sd_stream is a cudaStream_t (NULL = legacy default stream).  Every
  *    device call is stream-ordered and asynchronous; errors raised on the
  *    device (non-finite outer gradients, NCCL async errors) surface at
@@ -142,6 +145,17 @@ sd_status sd_get_unique_id(uint8_t id[SD_UNIQUE_ID_BYTES]);
  * NCCL communicator init).  Creates a highest-priority comm stream.  */
 sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, const uint8_t* id,
                   int32_t device);
+
+/* Allocates a gather buffer for a fragment of n elements: M payloads,
+ * 256-byte aligned.  With a communicator: NCCL symmetric memory
+ * (ncclMemAlloc) registered as a symmetric window of the ctx's communicator
+ * -- COLLECTIVE: every rank calls it in the same order with the same n --
+ * so sd_fragment_sync's all-gather runs on the copy engines
+ * (NCCL_CTA_POLICY_ZERO), leaving every SM to the compute stream.  Without a
+ * communicator: plain device memory.  Freed by sd_gather_free (collective
+ * with a communicator) or sd_finalize. */
+sd_status sd_gather_alloc(sd_ctx* ctx, int64_t n, void** out);
+sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
 
 /* Outer-state store init (§8(a) a2; AMB-2): anchor <- theta, momentum <- 0. */
 sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, float* momentum,

@@ -125,8 +125,16 @@ struct Inflight {
 
 }  // namespace
 
+struct GatherBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ncclWindow_t win = nullptr;
+  bool nccl = false;
+};
+
 struct sd_ctx {
   sd_config cfg;
+  std::vector<GatherBuf> bufs;
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -320,7 +328,10 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   if (id && M > 1) {
     ncclUniqueId u;
     memcpy(u.internal, id, SD_UNIQUE_ID_BYTES);
-    ncclResult_t r = ncclCommInitRank(&c->comm, M, u, rank);
+    // copy-engine collectives on symmetric windows: the gather takes no SMs
+    ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+    ncfg.CTAPolicy = NCCL_CTA_POLICY_ZERO;
+    ncclResult_t r = ncclCommInitRankConfig(&c->comm, M, u, rank, &ncfg);
     if (r != ncclSuccess) {
       c->comm = nullptr;
       fail(g_err, SD_ERR_NCCL, "ncclCommInitRank(M=%d, rank=%d): %s", M, rank, ncclGetErrorString(r));
@@ -329,6 +340,57 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   }
   *out = c;
   return SD_OK;
+}
+
+sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (!out) return ctx_fail(c, SD_ERR_ARG, "out pointer is NULL");
+  *out = nullptr;
+  if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
+  SD_CUDA(c, cudaSetDevice(c->device));
+  GatherBuf b;
+  b.bytes = (size_t)align_up((int64_t)(payload_of(&c->cfg, n).bytes * (size_t)c->M), 2 << 20);
+  if (c->comm) {
+    ncclResult_t r = ncclMemAlloc(&b.ptr, b.bytes);
+    if (r != ncclSuccess) return ctx_fail(c, SD_ERR_NCCL, "ncclMemAlloc(%zu): %s", b.bytes, ncclGetErrorString(r));
+    r = ncclCommWindowRegister(c->comm, b.ptr, b.bytes, &b.win, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+      ncclMemFree(b.ptr);
+      return ctx_fail(c, SD_ERR_NCCL, "ncclCommWindowRegister(%zu): %s", b.bytes, ncclGetErrorString(r));
+    }
+    b.nccl = true;
+  } else {
+    SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
+  }
+  c->bufs.push_back(b);
+  *out = b.ptr;
+  return SD_OK;
+}
+
+namespace {
+void release(sd_ctx* c, GatherBuf& b) {
+  if (b.nccl) {
+    if (b.win) ncclCommWindowDeregister(c->comm, b.win);
+    ncclMemFree(b.ptr);
+  } else if (b.ptr) {
+    cudaFree(b.ptr);
+  }
+  b = GatherBuf();
+}
+}  // namespace
+
+sd_status sd_gather_free(sd_ctx* c, void* gather_buf) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  for (size_t i = 0; i < c->bufs.size(); ++i) {
+    if (c->bufs[i].ptr == gather_buf) {
+      SD_CUDA(c, cudaSetDevice(c->device));
+      SD_CUDA(c, cudaDeviceSynchronize());
+      release(c, c->bufs[i]);
+      c->bufs.erase(c->bufs.begin() + (long)i);
+      return SD_OK;
+    }
+  }
+  return ctx_fail(c, SD_ERR_ARG, "gather_buf %p was not allocated by sd_gather_alloc on this ctx", gather_buf);
 }
 
 sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, float* momentum, int64_t n,
@@ -480,6 +542,9 @@ const char* sd_last_error(const sd_ctx* c) { return c ? c->err : g_err; }
 sd_status sd_finalize(sd_ctx* c) {
   if (!c) return SD_OK;
   cudaSetDevice(c->device);
+  if (!c->bufs.empty()) cudaDeviceSynchronize();
+  for (GatherBuf& b : c->bufs) release(c, b);
+  c->bufs.clear();
   if (c->comm) {
     ncclCommDestroy(c->comm);
     c->comm = nullptr;

@@ -26,7 +26,8 @@ STATUS_NAMES = {
 EXPORTS = (
     "sd_config_default", "sd_config_validate", "sd_fragment_count", "sd_fragment_layout",
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
-    "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_outer_state_init",
+    "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free",
+    "sd_outer_state_init",
     "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
@@ -73,6 +74,8 @@ def lib():
             "sd_payload_trailer_offset": ([C, I64], SZ),
             "sd_get_unique_id": ([P], I32),
             "sd_init": ([ctypes.POINTER(P), C, I32, I32, P, I32], I32),
+            "sd_gather_alloc": ([P, I64, ctypes.POINTER(P)], I32),
+            "sd_gather_free": ([P, P], I32),
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
             "sd_outer_grad_quantize": ([P, I32, I64, P, P, I64, P, P], I32),
             "sd_fragment_sync": ([P, I32, I64, P, I64, P], I32),
@@ -186,6 +189,21 @@ def _stream(stream):
     return ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
 
 
+class _CudaBytes:
+    """__cuda_array_interface__ view of raw device memory (libsd-owned)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def _device_bytes(ptr: int, nbytes: int, device: int):
+    import torch
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaBytes(ptr, nbytes), device=torch.device("cuda", device))
+
+
 class SdContext:
     """One replica's libsd context (sd_init ... sd_finalize)."""
 
@@ -201,6 +219,16 @@ class SdContext:
 
     def _c(self, st):
         _check(st, self.h)
+
+    def sd_gather_alloc(self, n: int, device=None):
+        """-> uint8 torch tensor view (M payloads) of a libsd-owned gather buffer"""
+        ptr = ctypes.c_void_p()
+        self._c(lib().sd_gather_alloc(self.h, n, ctypes.byref(ptr)))
+        nbytes = self.M * sd_payload_bytes(self.cfg, n)
+        return _device_bytes(ptr.value, nbytes, self.device if device is None else device)
+
+    def sd_gather_free(self, buf):
+        self._c(lib().sd_gather_free(self.h, _ptr(buf)))
 
     def sd_outer_state_init(self, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n

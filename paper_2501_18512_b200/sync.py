@@ -1,14 +1,13 @@
 """FragmentSync: one replica's side of Alg. 2's outer synchronization.
 
-Owns the libsd context and the per-fragment gather buffers (torch device
-memory) and issues the C-ABI calls in the paper's order at a step t:
+Owns the libsd context and the per-fragment gather buffers (allocated by
+libsd: NCCL symmetric memory, so the all-gather runs on the copy engines)
+and issues the C-ABI calls in the paper's order at a step t:
 sends first (Alg. 2 L6-8: sd_outer_grad_quantize + sd_fragment_sync), then
 receives (L10-13: sd_merge).  torch supplies memory, streams and the
 process group that broadcasts the NCCL unique id; nothing here computes.
 """
 from __future__ import annotations
-
-import torch
 
 from . import sd
 
@@ -30,8 +29,9 @@ class FragmentSync:
             unique_id = obj[0]
         self.ctx = sd.SdContext(cfg, rank, world, unique_id if world > 1 else None, device)
         self.payload = [sd.sd_payload_bytes(cfg, n) for n in self.n]
-        dev = torch.device("cuda", device)
-        self.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in self.payload]
+        # libsd-owned gather buffers: NCCL symmetric memory (copy-engine all-gather, zero SMs)
+        # with a communicator; plain device memory otherwise
+        self.gather = [self.ctx.sd_gather_alloc(n) for n in self.n]
 
     def slot(self, p: int) -> torch.Tensor:
         pb = self.payload[p]
@@ -62,4 +62,5 @@ class FragmentSync:
         return self.ctx.sd_check()
 
     def close(self):
+        self.gather = []
         self.ctx.sd_finalize()

@@ -35,6 +35,8 @@ def main():
     p = 2
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)
     fsync = FragmentSync(cfg, [n] * P, rank, world, local)
+    if os.environ.get("SD_TEST_TORCH_BUF") == "1":  # caller-owned (non-symmetric) gather buffers
+        fsync.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in fsync.payload]
     A = synth.dev_init(torch.empty(n, device=dev), segs, p)
     v = torch.zeros(n, device=dev)
     th = A.clone()

@@ -23,19 +23,20 @@ def _free_port():
     return port
 
 
-def _run(nproc, B):
-    env = dict(os.environ, SD_TEST_B=str(B))
+def _run(nproc, B, torch_buf=False):
+    env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     return r.returncode, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("B", [1024, 0])
-def test_nccl_allgather_two_ranks_bit_exact(B):
+@pytest.mark.parametrize("B,torch_buf", [(1024, False), (0, False), (1024, True)])
+def test_nccl_allgather_two_ranks_bit_exact(B, torch_buf):
+    """symmetric libsd buffers (copy-engine gather) and caller-owned torch buffers"""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    rc, out = _run(2, B)
+    rc, out = _run(2, B, torch_buf)
     assert rc == 0 and "OK" in out, out[-3000:]
 
 
