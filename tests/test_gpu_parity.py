@@ -308,3 +308,27 @@ def test_full_size_sampled_blocks(shape):
             assert_same(v_d[m][lo:hi], vo, f"block {b} momentum")
             assert_same(th_d[m][lo:hi], merges[m], f"block {b} theta")
     rep.close()
+
+
+def test_gather_alloc_single_gpu_and_free_errors():
+    """sd_gather_alloc without a communicator: plain device memory, usable by
+    the round; freeing a pointer it did not allocate is SD_ERR_ARG."""
+    n, M = 3000, 1
+    cfg = cfg_for(1024)
+    ctx = sd.SdContext(cfg, 0, M, None, 0)
+    buf = ctx.sd_gather_alloc(n)
+    assert buf.numel() == M * sd.sd_payload_bytes(cfg, n) and buf.data_ptr() % 256 == 0
+    A0 = (np.arange(n, dtype=np.float32) * 1e-3).astype(np.float32)
+    th = (A0 - np.float32(1e-4)).astype(np.float32)
+    A_d, v_d, th_d = to_dev(A0), torch.zeros(n, device=DEV), to_dev(th)
+    ctx.sd_outer_grad_quantize(0, 10, th_d, A_d, buf, n)
+    ctx.sd_fragment_sync(0, 10, buf, n)
+    ctx.sd_merge(0, 11, buf, th_d, A_d, v_d, n)
+    torch.cuda.synchronize()
+    want, _ = oracle.quantize(th, A0, 1024)
+    assert np.array_equal(buf.cpu().numpy(), want)
+    with pytest.raises(sd.SdError) as e:
+        ctx.sd_gather_free(torch.empty(256, dtype=torch.uint8, device=DEV))
+    assert e.value.status == sd.SD_ERR_ARG
+    ctx.sd_gather_free(buf)
+    ctx.sd_finalize()
