@@ -29,6 +29,7 @@
 #include <float.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sd_kernels.h"
 
@@ -468,29 +469,26 @@ int ilog2_or_neg(int32_t B) {
   return l;
 }
 
-// resident blocks per SM of a kernel, queried once per kernel
-int occupancy(const void* kernel) {
-  static const void* keys[32];
-  static int vals[32];
-  static int used = 0;
-  for (int i = 0; i < used; ++i)
-    if (keys[i] == kernel) return vals[i];
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
-  if (used < 32) {
-    keys[used] = kernel;
-    vals[used] = occ;
-    ++used;
+// Grid sizing.  Measured on B200 (scripts/gpu_grid_sweep.sh, 1B fragments):
+// one CTA per tile of work (no grid-stride iterations) beats a persistent
+// SMs x occupancy grid by ~8% (apply) / ~10% (quantize) -- the resident CTAs
+// then cover a compact, advancing address window, which keeps DRAM pages
+// open.  SD_BLOCKS_PER_SM=<k> caps the grid at k CTAs per SM (experiments).
+int blocks_per_sm_cap() {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("SD_BLOCKS_PER_SM");
+    cap = e ? atoi(e) : 0;
   }
-  return occ;
+  return cap;
 }
 
 template <typename K>
 int grid_for(K kernel, int num_sms, int64_t work_items, int items_per_block) {
-  const int occ = occupancy(reinterpret_cast<const void*>(kernel));
-  int64_t need = (work_items + items_per_block - 1) / items_per_block;
-  int64_t g = (int64_t)num_sms * occ;
-  if (need < g) g = need;
+  (void)kernel;
+  int64_t g = (work_items + items_per_block - 1) / items_per_block;
+  if (blocks_per_sm_cap() > 0 && g > (int64_t)num_sms * blocks_per_sm_cap()) g = (int64_t)num_sms * blocks_per_sm_cap();
+  if (g > 0x7fffffffLL) g = 0x7fffffffLL;
   return g < 1 ? 1 : (int)g;
 }
 
