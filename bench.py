@@ -48,8 +48,8 @@ def peaks():
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
-    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="1B", choices=["toy", "35M", "1B", "4B"])
     ap.add_argument("--scale-block", type=int, default=1024)
@@ -317,6 +317,13 @@ def main():
     pipelined = P > 1 and not args.serial
     step_fn = pipe_step if pipelined else one_step
 
+    # L2 policy: the 1B/4B state (12 B/param, GBs) streams through HBM; small
+    # configs (toy, 35M) would stay L2-resident, so they flush L2 between steps
+    # and time only the steps (sum of per-step event intervals).
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = 12 * sum(n) < 4 * l2_bytes
+    flush_buf = torch.empty(2 * l2_bytes, dtype=torch.uint8, device=dev) if flush else None
+
     def timed(evs, fn):
         for p, t in evs[:W]:
             fn(p, t)
@@ -324,13 +331,19 @@ def main():
         if world > 1:
             dist.barrier()
         kev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = sd.sd_kernel_launch_count()
         torch.cuda.synchronize()
         t0 = time.time()
         start.record()
         for i, (p, t) in enumerate(evs[W:]):
+            if flush:
+                flush_buf.zero_()
+                sev[i][0].record()
             fn(p, t, kev[i])
+            if flush:
+                sev[i][1].record()
         stop.record()
         torch.cuda.synchronize()
         t1 = time.time()
@@ -339,7 +352,8 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return start.elapsed_time(stop), kev, nl, t0, t1
+        total = sum(a.elapsed_time(b) for a, b in sev) if flush else start.elapsed_time(stop)
+        return total, kev, nl, t0, t1
 
     ms, kev, launches, w0, w1 = timed(events, step_fn)
     launches0 = 0
@@ -414,8 +428,12 @@ def main():
     # ---- gather hidden behind tau synthetic inner steps? (N > 1 only)
     overlap = None
     if world > 1:
-        more = calendar_sends(sd, cfg, 3 * (W + K) + 12)[2 * (W + K):]
-        overlap = overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, more, dev)
+        overlap = {}
+        for i, kind in enumerate(("adamw", "gemm")):
+            base = 5 * (W + K) + 24 * i
+            evs = calendar_sends(sd, cfg, base + 24)[base:]
+            overlap[kind] = overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, evs, dev,
+                                        kind=kind)
 
     # ---- per-GPU kernel work at M = 1/2/4/8 replicas, emulated on this GPU (1 fragment)
     m_sweep = None
@@ -432,7 +450,11 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
-            "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n]),
+            "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n],
+                           l2=("state (12 B/param) fits in ~4x L2: L2 flushed (2x L2 written) between steps, "
+                               "only the steps are timed" if flush else
+                               "inputs > L2 (fragments of %.0f-%.0f MB per fp32 array, cycled); no flush"
+                               % (4 * min(n) / 1e6, 4 * max(n) / 1e6))),
             "per_gpu_value": value / world,
             "schedule": ("pipelined: each step sends fragment k (quantize + async NCCL all-gather) and receives "
                          "fragment k-1 (block-receive + apply), so a gather overlaps the next step's kernels "
@@ -463,26 +485,38 @@ def main():
     return 0
 
 
-def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=4):
+def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=4,
+                kind="adamw"):
     """SURVEY.md §8(d) hidden-gather check on the real NCCL path: per round,
     quantize -> all-gather on the comm stream while the compute stream runs
-    tau AdamW-shaped synthetic inner steps over the whole replica (24 B/param)
-    -> block-receive -> apply.  exposed = window with the gather in flight -
-    the same tau inner steps alone; hidden <=> exposed <= 5% of the gather
-    measured alone.  All times: CUDA events on the compute stream, max over
-    ranks."""
+    tau synthetic inner steps -> block-receive -> apply.  exposed = window
+    with the gather in flight - the same tau inner steps alone; hidden <=>
+    exposed <= 5% of the gather measured alone.  Two inner-step kinds:
+    "adamw" = an AdamW-shaped pass over the whole replica (24 B/param, HBM-
+    bound: the worst case for the gather's own HBM traffic) and "gemm" =
+    bf16 cuBLAS matmuls (SM-bound).  CUDA events on the compute stream, max
+    over ranks."""
     import statistics as st
 
-    m1 = [torch.zeros_like(x) for x in theta]
-    m2 = [torch.zeros_like(x) for x in theta]
     tau = cfg.tau
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     step = [1]
+    if kind == "adamw":
+        m1 = [torch.zeros_like(x) for x in theta]
+        m2 = [torch.zeros_like(x) for x in theta]
 
-    def inner():
-        for p in range(P):
-            synth.dev_inner_adamw(theta[p], m1[p], m2[p], rank, step[0])
-        step[0] += 1
+        def inner():
+            for p in range(P):
+                synth.dev_inner_adamw(theta[p], m1[p], m2[p], rank, step[0])
+            step[0] += 1
+    else:
+        X = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+        Wm = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+        Y = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+
+        def inner():
+            for _ in range(4):
+                torch.matmul(X, Wm, out=Y)
 
     def maxr(x):
         t = torch.tensor([x], device=dev)
@@ -524,7 +558,8 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
     ta, tg, to = st.median(alone), st.median(gath), st.median(over)
     exposed = max(0.0, to - ta)
     gbps = st.median(bytes_in) / (tg / 1e3) / 1e9
-    return {"tau": tau, "inner_step": "AdamW-shaped synthetic pass over the whole replica, 24 B/param (synth/)",
+    return {"tau": tau, "inner_step": ("AdamW-shaped synthetic pass over the whole replica, 24 B/param (synth/)"
+                                       if kind == "adamw" else "4 bf16 8192^3 cuBLAS matmuls (SM-bound)"),
             "inner_window_ms": ta, "overlap_window_ms": to, "gather_alone_ms": tg, "exposed_ms": exposed,
             "hidden": exposed <= 0.05 * tg, "inner_slowdown": to / ta if ta > 0 else None,
             "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,

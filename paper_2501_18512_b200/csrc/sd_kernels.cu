@@ -322,7 +322,29 @@ __global__ void __launch_bounds__(kThreads) k_absmax(QArgs a) {
   uint32_t run = 0;
   for (int64_t c = warp; c < nfull; c += nwarps) absmax_chunk<true>(a, c, lane, cur, run);
   if ((nfull << 10) < a.n && warp == nfull % nwarps) absmax_chunk<false>(a, nfull, lane, cur, run);
-  if (cur >= 0 && lane == 0) atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + cur, run);
+  // merge the CTA's warps that ended in the same block: one atomic per distinct
+  // block per CTA (B = 0: one per CTA instead of one per warp)
+  __shared__ int64_t s_blk[kThreads / 32];
+  __shared__ uint32_t s_run[kThreads / 32];
+  if (lane == 0) {
+    s_blk[threadIdx.x >> 5] = cur;
+    s_run[threadIdx.x >> 5] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t b = -1;
+    uint32_t r = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      if (s_blk[w] < 0) continue;
+      if (s_blk[w] != b) {
+        if (b >= 0) atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + b, r);
+        b = s_blk[w];
+        r = 0;
+      }
+      r = max(r, s_run[w]);
+    }
+    if (b >= 0) atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + b, r);
+  }
 }
 
 template <bool kFullChunk>
