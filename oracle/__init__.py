@@ -59,6 +59,7 @@ def lib():
             "or_apply": ([P, I32, I64, I32, F, F, F, P, P, P], ctypes.c_int),
             "or_round": ([I32, I64, I32, F, F, F, P, P, P, P, P], ctypes.c_int),
             "or_toy_run": ([C, I32, I64, ctypes.c_uint64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
+            "or_toy_run_taus": ([C, I32, I64, ctypes.c_uint64, P, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -182,4 +183,17 @@ def toy_run(c: OrConfig, M: int, block_len: int, seed: int):
     v = np.empty(P * n, dtype=np.float32)
     bs = ctypes.c_int64(0)
     r = lib().or_toy_run(ctypes.byref(c), M, block_len, seed, _p(theta), _p(A), _p(v), ctypes.byref(bs))
+    return theta, A, v, bs.value, r
+
+
+def toy_run_taus(c: OrConfig, M: int, block_len: int, seed: int, taus):
+    """Per-replica tau_m -> (theta [M, P*n], A [M, P*n], v [M, P*n], bytes, status)"""
+    P = num_fragments(c)
+    n = c.fs * block_len
+    theta = np.empty((M, P * n), dtype=np.float32)
+    A = np.empty((M, P * n), dtype=np.float32)
+    v = np.empty((M, P * n), dtype=np.float32)
+    t = np.ascontiguousarray(taus, dtype=np.int32)
+    bs = ctypes.c_int64(0)
+    r = lib().or_toy_run_taus(ctypes.byref(c), M, block_len, seed, _p(t), _p(theta), _p(A), _p(v), ctypes.byref(bs))
     return theta, A, v, bs.value, r

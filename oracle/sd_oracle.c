@@ -340,3 +340,74 @@ int or_toy_run(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, 
   free(gather);
   return any_poison;
 }
+
+/* Per-replica overlap delay tau_m (Sec. 3.3.2 "Overlapping
+ * with some slack between workers": all replicas send at the same step, each
+ * receives tau_m steps later).  Same as or_toy_run but every
+ * replica keeps its own copy of the (replicated) anchor and momentum, applies
+ * OuterOpt at its own receive step and merges its own parameters then.
+ * A_m[m*Ntot + ...], v_m likewise.  Returns 0, or 1 if a round was poisoned. */
+int or_toy_run_taus(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, const int32_t* taus,
+                    float* theta, float* A_m, float* v_m, int64_t* bytes_sent) {
+  const int32_t P = or_num_fragments(c);
+  const int64_t n = (int64_t)c->fs * block_len;
+  const int64_t Ntot = (int64_t)P * n;
+  const size_t pb = or_payload_bytes(n, c->B);
+  uint8_t* gather = (uint8_t*)calloc((size_t)P * (size_t)M, pb);
+  or_event** ev = (or_event**)malloc(sizeof(or_event*) * (size_t)M);
+  int64_t* nev = (int64_t*)malloc(sizeof(int64_t) * (size_t)M);
+  int64_t* e = (int64_t*)calloc((size_t)M, sizeof(int64_t));
+  float* g = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  int any_poison = 0;
+  synth_segment seg;
+  *bytes_sent = 0;
+  for (int32_t m = 0; m < M; ++m) { /* each replica's own calendar: same sends, receives at s + tau_m */
+    or_config cm = *c;
+    cm.tau = taus[m];
+    nev[m] = or_calendar(&cm, NULL, 0);
+    ev[m] = (or_event*)malloc(sizeof(or_event) * (size_t)(nev[m] > 0 ? nev[m] : 1));
+    or_calendar(&cm, ev[m], nev[m]);
+  }
+  for (int32_t p = 0; p < P; ++p) {
+    seg.start = 0; seg.len = n; seg.kind = SYN_MATRIX; seg.first_block = 0; seg.row = 1; seg.pad_ = 0;
+    for (int64_t i = 0; i < n; ++i) A_m[p * n + i] = syn_init_value(&seg, seed, p, i);
+    for (int64_t i = 0; i < n; ++i) v_m[p * n + i] = 0.0f;
+  }
+  for (int32_t m = 1; m < M; ++m) {
+    memcpy(A_m + m * Ntot, A_m, sizeof(float) * (size_t)Ntot);
+    memcpy(v_m + m * Ntot, v_m, sizeof(float) * (size_t)Ntot);
+  }
+  for (int32_t m = 0; m < M; ++m) memcpy(theta + m * Ntot, A_m, sizeof(float) * (size_t)Ntot);
+
+  for (int64_t t = 1; t <= c->T; ++t) {
+    for (int32_t m = 0; m < M; ++m) /* L3-5 */
+      for (int64_t gi = 0; gi < Ntot; ++gi)
+        theta[m * Ntot + gi] = theta[m * Ntot + gi] - syn_toy_value(seed, m, t, gi);
+    /* L6-8: sends are common to all replicas (replica 0's calendar lists them) */
+    for (int64_t k = e[0]; k < nev[0] && ev[0][k].t == t; ++k) {
+      if (ev[0][k].kind != 0) continue;
+      const int32_t p = ev[0][k].p;
+      uint8_t* gp = gather + (size_t)p * (size_t)M * pb;
+      for (int32_t m = 0; m < M; ++m)
+        or_quantize(theta + m * Ntot + p * n, A_m + m * Ntot + p * n, n, c->B, gp + (size_t)m * pb);
+      *bytes_sent += (int64_t)M * (int64_t)pb;
+    }
+    /* L10-13 per replica at its own receive steps */
+    for (int32_t m = 0; m < M; ++m) {
+      for (; e[m] < nev[m] && ev[m][e[m]].t == t; ++e[m]) {
+        if (ev[m][e[m]].kind != 1) continue;
+        const int32_t p = ev[m][e[m]].p;
+        uint8_t* gp = gather + (size_t)p * (size_t)M * pb;
+        int skip = 0;
+        for (int32_t q = 0; q < M; ++q) skip |= or_payload_poisoned(gp + (size_t)q * pb, n, c->B, NULL) != 0;
+        if (skip) { any_poison = 1; continue; }
+        or_decode_mean(gp, M, n, c->B, g);
+        or_nesterov(A_m + m * Ntot + p * n, v_m + m * Ntot + p * n, g, n, c->lr, c->mu);
+        or_merge(theta + m * Ntot + p * n, A_m + m * Ntot + p * n, n, c->alpha);
+      }
+    }
+  }
+  for (int32_t m = 0; m < M; ++m) free(ev[m]);
+  free(ev); free(nev); free(e); free(g); free(gather);
+  return any_poison;
+}

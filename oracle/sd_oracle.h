@@ -71,4 +71,7 @@ int or_round(int32_t M, int64_t n, int32_t B, float lr, float mu, float alpha,
 int or_toy_run(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, float* theta,
                float* A, float* v, int64_t* bytes_sent);
 
+int or_toy_run_taus(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, const int32_t* taus,
+                    float* theta, float* A_m, float* v_m, int64_t* bytes_sent);
+
 #endif /* SD_ORACLE_H_ */

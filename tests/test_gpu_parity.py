@@ -332,3 +332,42 @@ def test_gather_alloc_single_gpu_and_free_errors():
     assert e.value.status == sd.SD_ERR_ARG
     ctx.sd_gather_free(buf)
     ctx.sd_finalize()
+
+
+def test_per_replica_tau_toy_run():
+    """NEXT-4: heterogeneous slack.  Replica m's context
+    is created with its own tau_m; all replicas send at the same steps, each
+    block-receives and merges tau_m steps later.  Final parameters, anchors and
+    momenta of both replicas bit-identical to or_toy_run_taus."""
+    M, bl, H, T, taus = 2, 1 << 16, 10, 60, [1, 5]
+    c_or = oracle.config(L=2, fs=1, H=H, tau=1, T=T)
+    th_o, A_o, v_o, sent_o, st = oracle.toy_run_taus(c_or, M, bl, synth.SEED, taus)
+    assert st == 0
+    cfgs = [sd.sd_config_default(2, 1, H, tau=taus[m], T=T) for m in range(M)]
+    P, n = sd.sd_fragment_count(cfgs[0]), bl
+    ctx = [sd.SdContext(cfgs[m], m, M, None, 0) for m in range(M)]
+    pb = sd.sd_payload_bytes(cfgs[0], n)
+    gather = [torch.empty(M * pb, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    A = [[synth.dev_init(torch.empty(n, device=DEV), synth.flat_segments(n), p) for p in range(P)] for _ in range(M)]
+    v = [[torch.zeros(n, device=DEV) for _ in range(P)] for _ in range(M)]
+    th = [torch.cat(A[0]).clone() for _ in range(M)]
+    for t in range(1, T + 1):
+        for m in range(M):
+            synth.dev_apply_toy(th[m], m, t)
+        sends = [sd.sd_fragment_schedule(cfgs[m], t)[0] for m in range(M)]
+        assert sends[0] == sends[1]  # same send steps for every replica
+        for p in sends[0]:
+            for m in range(M):
+                ctx[m].sd_outer_grad_quantize(p, t, th[m][p * n:(p + 1) * n], A[m][p], gather[p][m * pb:(m + 1) * pb], n)
+            for m in range(M):
+                ctx[m].sd_fragment_sync(p, t, gather[p], n)
+        for m in range(M):
+            for p in sd.sd_fragment_schedule(cfgs[m], t)[1]:
+                ctx[m].sd_merge(p, t, gather[p], th[m][p * n:(p + 1) * n], A[m][p], v[m][p], n)
+    torch.cuda.synchronize()
+    for m in range(M):
+        assert_same(th[m], th_o[m], f"theta replica {m}")
+        assert_same(torch.cat(A[m]), A_o[m], f"anchor replica {m}")
+        assert_same(torch.cat(v[m]), v_o[m], f"momentum replica {m}")
+    for c in ctx:
+        c.sd_finalize()

@@ -251,3 +251,28 @@ def test_toy_config_runs_and_keeps_outer_state_shared():
     assert st == 0 and np.all(np.isfinite(theta)) and v.any()
     sends = sum(1 for e in oracle.calendar(c) if e[1] == 0)
     assert sent == sends * 2 * oracle.payload_bytes(2 ** 19, 1024)
+
+
+def test_per_replica_tau_equal_taus_reduce_to_toy_run():
+    """NEXT-4: with tau_m = tau for every replica the
+    per-replica run is the plain Alg. 2 run bit for bit."""
+    c = oracle.config(L=2, fs=1, H=8, tau=2, T=41)
+    th1, A1, v1, b1, s1 = oracle.toy_run(c, 2, 3000, 7)
+    th2, A2, v2, b2, s2 = oracle.toy_run_taus(c, 2, 3000, 7, [2, 2])
+    assert s1 == s2 == 0 and b1 == b2
+    assert np.array_equal(bits(th1), bits(th2))
+    for m in range(2):
+        assert np.array_equal(bits(A2[m]), bits(A1)) and np.array_equal(bits(v2[m]), bits(v1))
+
+
+def test_per_replica_tau_slack_keeps_outer_state_replicated():
+    """tau_1 = 1, tau_2 = 5: both replicas send at the same
+    step and receive at their own; the outer state each holds is the same
+    after every completed round (flush at T), while the live parameters differ
+    from the equal-tau run (the slower replica merges later)."""
+    c = oracle.config(L=2, fs=1, H=10, tau=1, T=60)
+    th, A, v, b, st = oracle.toy_run_taus(c, 2, 2048, 11, [1, 5])
+    assert st == 0
+    assert np.array_equal(bits(A[0]), bits(A[1])) and np.array_equal(bits(v[0]), bits(v[1]))
+    th_eq, A_eq, _, _, _ = oracle.toy_run(c, 2, 2048, 11)
+    assert not np.array_equal(bits(th[1]), bits(th_eq[1]))
