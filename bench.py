@@ -440,6 +440,11 @@ def main():
     if world == 1 and not args.no_m_sweep:
         m_sweep = m_sweep_run(torch, sd, synth, cfg, segs[0], n[0], B, dev, peak)
 
+    # ---- NEXT-3: host-offloaded outer state -- transfer cost of one fragment's A, v
+    offload = None
+    if world == 1 and not args.no_e2e:
+        offload = offload_run(torch, sync, A[0], v[0], n, P, dev)
+
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, B, M, segs[0], n[0], args.cpu_seconds)
@@ -477,6 +482,7 @@ def main():
             "cpu_baseline": cpu,
             "m_sweep_emulated": m_sweep,
             "overlap": overlap,
+            "offload": offload,
         }
         print(json.dumps(line))
     sync.close()
@@ -564,6 +570,37 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
             "hidden": exposed <= 0.05 * tg, "inner_slowdown": to / ta if ta > 0 else None,
             "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,
                        "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0}}
+
+
+def offload_run(torch, sync, A0, v0, n, P, dev, reps=5):
+    """Outer state offloaded to pinned host memory (sd_state_prefetch /
+    sd_state_writeback): time to move fragment 0's anchor +
+    momentum (8 B/param) H2D and D2H on libsd's copy stream."""
+    import statistics as st
+
+    ctx = sync.ctx
+    hA = torch.empty(n[0], dtype=torch.float32, pin_memory=True)
+    hv = torch.empty(n[0], dtype=torch.float32, pin_memory=True)
+    pre, wb = [], []
+    for r in range(reps + 1):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        ctx.sd_state_writeback(0, A0, v0, hA, hv, n[0])
+        ctx.sd_state_sync()
+        e[1].record()
+        ctx.sd_state_prefetch(0, hA, hv, A0, v0, n[0])
+        ctx.sd_state_sync()
+        e[2].record()
+        torch.cuda.synchronize()
+        if r:
+            wb.append(e[0].elapsed_time(e[1]))
+            pre.append(e[1].elapsed_time(e[2]))
+    tp, tw = st.median(pre), st.median(wb)
+    nbytes = 8 * n[0]
+    return {"fragment_elems": int(n[0]), "bytes_each_way": int(nbytes), "prefetch_ms": tp, "writeback_ms": tw,
+            "H2D_GBps": nbytes / (tp / 1e3) / 1e9, "D2H_GBps": nbytes / (tw / 1e3) / 1e9,
+            "paper_claim": "< 10 ms per fragment + outer state on an H100 (PAPER.md:149)",
+            "hbm_outer_state_bytes": {"resident": int(8 * sum(n)), "offloaded_two_slots": int(2 * 8 * max(n))}}
 
 
 def m_sweep_run(torch, sd, synth, cfg, segs, n, B, dev, peak, iters=12):

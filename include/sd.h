@@ -161,6 +161,27 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
 sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, float* momentum,
                               int64_t n, sd_stream stream);
 
+/* Host-offloaded outer-state store (PAPER.md:145-149:
+ * "only a subset of the outer parameters and outer optimizer state is needed
+ * at a given time ... we can start the transfer from RAM to HBM of a fragment
+ * ... while finishing the previous (inner) gradients passes").  A_p and v_p
+ * live in (pinned) host memory; `anchor`/`momentum` are device staging
+ * buffers of n floats (HBM holds 2 x |p| instead of 2 x the model).
+ *  sd_state_prefetch: after `stream`'s prior work (the staging buffers' last
+ *    user), H2D copies on the ctx's copy stream; the next
+ *    sd_outer_grad_quantize of p waits for them.  p must not be in flight.
+ *  sd_state_writeback: after `stream`'s prior work (the merge of p), D2H
+ *    copies on the copy stream.  p must not be in flight.
+ *  sd_state_sync: `stream` waits for every copy issued so far (e.g. before
+ *    reading the host store or reusing the host buffers).
+ * Copies are FIFO on one copy stream, so a prefetch into a staging buffer
+ * never overtakes the writeback of its previous contents. */
+sd_status sd_state_prefetch(sd_ctx* ctx, int32_t p, const float* anchor_host, const float* momentum_host,
+                            float* anchor, float* momentum, int64_t n, sd_stream stream);
+sd_status sd_state_writeback(sd_ctx* ctx, int32_t p, const float* anchor, const float* momentum,
+                             float* anchor_host, float* momentum_host, int64_t n, sd_stream stream);
+sd_status sd_state_sync(sd_ctx* ctx, sd_stream stream);
+
 /* Alg. 2 L7 + E3M0 (§8(a) a3).  p must be scheduled to send at t and not be
  * in flight.  Reads theta[n], anchor[n]; writes one payload
  * (sd_payload_bytes) at slot_out, which must be gather_buf + rank * payload

@@ -138,7 +138,11 @@ struct sd_ctx {
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;               // outer-state offload (NEXT-3)
   std::vector<cudaEvent_t> ready, done;
+  std::vector<cudaEvent_t> staged;                   // prefetch of fragment p landed
+  std::vector<char> prefetch_pending;                // quantize must wait on staged[p]
+  cudaEvent_t copy_gate = nullptr;
   std::vector<Inflight> fl;
   unsigned long long* status_host = nullptr;  // {first_bad, flags}: pinned, mapped
   unsigned long long* status_dev = nullptr;
@@ -312,6 +316,16 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   e = cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreateWithPriority"));
+  e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreate(copy)"));
+  e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaEventCreate(copy_gate)"));
+  c->staged.assign((size_t)c->P, nullptr);
+  c->prefetch_pending.assign((size_t)c->P, 0);
+  for (int32_t p = 0; p < c->P; ++p) {
+    e = cudaEventCreateWithFlags(&c->staged[p], cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaEventCreate(staged)"));
+  }
   c->ready.assign((size_t)c->P, nullptr);
   c->done.assign((size_t)c->P, nullptr);
   for (int32_t p = 0; p < c->P; ++p) {
@@ -393,6 +407,55 @@ sd_status sd_gather_free(sd_ctx* c, void* gather_buf) {
   return ctx_fail(c, SD_ERR_ARG, "gather_buf %p was not allocated by sd_gather_alloc on this ctx", gather_buf);
 }
 
+sd_status sd_state_prefetch(sd_ctx* c, int32_t p, const float* anchor_host, const float* momentum_host,
+                            float* anchor, float* momentum, int64_t n, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, 1, n))) return st;
+  if (c->fl[p].state != IDLE)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d is in flight: its outer state is in use", p);
+  if (n == 0) return SD_OK;
+  if ((st = check_ptr(c, anchor_host, 4, "anchor_host")) || (st = check_ptr(c, momentum_host, 4, "momentum_host")) ||
+      (st = check_ptr(c, anchor, 32, "anchor")) || (st = check_ptr(c, momentum, 32, "momentum")))
+    return st;
+  SD_CUDA(c, cudaSetDevice(c->device));
+  // the staging slot is free once `stream`'s prior work (the last user of the slot) is done
+  SD_CUDA(c, cudaEventRecord(c->copy_gate, static_cast<cudaStream_t>(stream)));
+  SD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
+  SD_CUDA(c, cudaMemcpyAsync(anchor, anchor_host, 4 * (size_t)n, cudaMemcpyHostToDevice, c->copy_stream));
+  SD_CUDA(c, cudaMemcpyAsync(momentum, momentum_host, 4 * (size_t)n, cudaMemcpyHostToDevice, c->copy_stream));
+  SD_CUDA(c, cudaEventRecord(c->staged[p], c->copy_stream));
+  c->prefetch_pending[p] = 1;
+  return SD_OK;
+}
+
+sd_status sd_state_writeback(sd_ctx* c, int32_t p, const float* anchor, const float* momentum, float* anchor_host,
+                             float* momentum_host, int64_t n, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sd_status st;
+  if ((st = check_fragment(c, p, 1, n))) return st;
+  if (c->fl[p].state != IDLE)
+    return ctx_fail(c, SD_ERR_STATE, "fragment %d is in flight: merge it before writing its state back", p);
+  if (n == 0) return SD_OK;
+  if ((st = check_ptr(c, anchor_host, 4, "anchor_host")) || (st = check_ptr(c, momentum_host, 4, "momentum_host")) ||
+      (st = check_ptr(c, anchor, 32, "anchor")) || (st = check_ptr(c, momentum, 32, "momentum")))
+    return st;
+  SD_CUDA(c, cudaSetDevice(c->device));
+  SD_CUDA(c, cudaEventRecord(c->copy_gate, static_cast<cudaStream_t>(stream)));  // after the merge
+  SD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
+  SD_CUDA(c, cudaMemcpyAsync(anchor_host, anchor, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->copy_stream));
+  SD_CUDA(c, cudaMemcpyAsync(momentum_host, momentum, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->copy_stream));
+  return SD_OK;
+}
+
+sd_status sd_state_sync(sd_ctx* c, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  SD_CUDA(c, cudaSetDevice(c->device));
+  SD_CUDA(c, cudaEventRecord(c->copy_gate, c->copy_stream));
+  SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->copy_gate, 0));
+  return SD_OK;
+}
+
 sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, float* momentum, int64_t n,
                               sd_stream stream) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
@@ -426,6 +489,10 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
   uint8_t* slot = static_cast<uint8_t*>(slot_out);
+  if (c->prefetch_pending[p]) {  // offloaded outer state: the anchor must have landed
+    SD_CUDA(c, cudaStreamWaitEvent(s, c->staged[p], 0));
+    c->prefetch_pending[p] = 0;
+  }
   SD_CUDA(c, cudaMemsetAsync(slot + pl.trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64 - 1
   const int k = sdk::launch_quantize(theta, anchor, pl, slot, c->num_sms, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
@@ -554,6 +621,10 @@ sd_status sd_finalize(sd_ctx* c) {
   for (cudaEvent_t e : c->done)
     if (e) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (cudaEvent_t e : c->staged)
+    if (e) cudaEventDestroy(e);
+  if (c->copy_gate) cudaEventDestroy(c->copy_gate);
   if (c->status_host) cudaFreeHost(c->status_host);
   delete c;
   return SD_OK;

@@ -27,7 +27,7 @@ EXPORTS = (
     "sd_config_default", "sd_config_validate", "sd_fragment_count", "sd_fragment_layout",
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free",
-    "sd_outer_state_init",
+    "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync",
     "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
@@ -77,6 +77,9 @@ def lib():
             "sd_gather_alloc": ([P, I64, ctypes.POINTER(P)], I32),
             "sd_gather_free": ([P, P], I32),
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
+            "sd_state_prefetch": ([P, I32, P, P, P, P, I64, P], I32),
+            "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
+            "sd_state_sync": ([P, P], I32),
             "sd_outer_grad_quantize": ([P, I32, I64, P, P, I64, P, P], I32),
             "sd_fragment_sync": ([P, I32, I64, P, I64, P], I32),
             "sd_fragment_wait": ([P, I32, I64, P], I32),
@@ -229,6 +232,19 @@ class SdContext:
 
     def sd_gather_free(self, buf):
         self._c(lib().sd_gather_free(self.h, _ptr(buf)))
+
+    def sd_state_prefetch(self, p, anchor_host, momentum_host, anchor, momentum, n=None, stream=None):
+        n = anchor.numel() if n is None else n
+        self._c(lib().sd_state_prefetch(self.h, p, _ptr(anchor_host), _ptr(momentum_host), _ptr(anchor),
+                                        _ptr(momentum), n, _stream(stream)))
+
+    def sd_state_writeback(self, p, anchor, momentum, anchor_host, momentum_host, n=None, stream=None):
+        n = anchor.numel() if n is None else n
+        self._c(lib().sd_state_writeback(self.h, p, _ptr(anchor), _ptr(momentum), _ptr(anchor_host),
+                                         _ptr(momentum_host), n, _stream(stream)))
+
+    def sd_state_sync(self, stream=None):
+        self._c(lib().sd_state_sync(self.h, _stream(stream)))
 
     def sd_outer_state_init(self, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n

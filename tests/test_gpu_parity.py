@@ -371,3 +371,55 @@ def test_per_replica_tau_toy_run():
         assert_same(torch.cat(v[m]), v_o[m], f"momentum replica {m}")
     for c in ctx:
         c.sd_finalize()
+
+
+def test_offloaded_outer_state_toy_run():
+    """NEXT-3: anchors and momenta of all fragments live in
+    pinned host memory; HBM holds two staging slots.  Each fragment's state is
+    prefetched two steps before its send and written back after its merge.
+    Result bit-identical to the resident-state oracle run (or_toy_run)."""
+    M, bl, H, tau, T = 2, 1 << 15, 12, 3, 80
+    c_or = oracle.config(L=4, fs=1, H=H, tau=tau, T=T)
+    th_o, A_o, v_o, _, st = oracle.toy_run(c_or, M, bl, synth.SEED)
+    assert st == 0
+    cfg = sd.sd_config_default(4, 1, H, tau=tau, T=T)
+    P, n = sd.sd_fragment_count(cfg), bl
+    ctx = [sd.SdContext(cfg, m, M, None, 0) for m in range(M)]
+    pb = sd.sd_payload_bytes(cfg, n)
+    gather = [torch.empty(M * pb, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    # host store (per replica, as on separate GPUs) and 2 device staging slots per replica
+    A_h = [[synth.dev_init(torch.empty(n, device=DEV), synth.flat_segments(n), p).cpu().pin_memory() for p in range(P)]
+           for _ in range(M)]
+    v_h = [[torch.zeros(n).pin_memory() for _ in range(P)] for _ in range(M)]
+    A_s = [[torch.empty(n, device=DEV) for _ in range(2)] for _ in range(M)]
+    v_s = [[torch.empty(n, device=DEV) for _ in range(2)] for _ in range(M)]
+    th = [torch.cat([A_h[0][p] for p in range(P)]).to(DEV) for _ in range(M)]
+    sends = {}
+    for t in range(1, T + 3):
+        s_ahead, _ = sd.sd_fragment_schedule(cfg, t + 2) if t + 2 <= T else ([], [])
+        for p in s_ahead:  # prefetch two steps ahead of the send
+            for m in range(M):
+                ctx[m].sd_state_prefetch(p, A_h[m][p], v_h[m][p], A_s[m][p % 2], v_s[m][p % 2], n)
+        if t > T:
+            continue
+        for m in range(M):
+            synth.dev_apply_toy(th[m], m, t)
+        send, recv = sd.sd_fragment_schedule(cfg, t)
+        for p in send:
+            for m in range(M):
+                ctx[m].sd_outer_grad_quantize(p, t, th[m][p * n:(p + 1) * n], A_s[m][p % 2], gather[p][m * pb:(m + 1) * pb], n)
+            for m in range(M):
+                ctx[m].sd_fragment_sync(p, t, gather[p], n)
+        for p in recv:
+            for m in range(M):
+                ctx[m].sd_merge(p, t, gather[p], th[m][p * n:(p + 1) * n], A_s[m][p % 2], v_s[m][p % 2], n)
+                ctx[m].sd_state_writeback(p, A_s[m][p % 2], v_s[m][p % 2], A_h[m][p], v_h[m][p], n)
+    for m in range(M):
+        ctx[m].sd_state_sync()
+    torch.cuda.synchronize()
+    for m in range(M):
+        assert_same(th[m], th_o[m], f"theta replica {m}")
+        assert_same(torch.cat(A_h[m]), A_o, f"host anchor store replica {m}")
+        assert_same(torch.cat(v_h[m]), v_o, f"host momentum store replica {m}")
+    for c in ctx:
+        c.sd_finalize()
