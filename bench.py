@@ -440,6 +440,11 @@ def main():
     if world == 1 and not args.no_m_sweep:
         m_sweep = m_sweep_run(torch, sd, synth, cfg, segs[0], n[0], B, dev, peak)
 
+    # ---- NEXT-1: the inner AdamW step before a send, separate vs fused with the quantize
+    fused = None
+    if world == 1 and not args.no_m_sweep:
+        fused = fused_inner_run(torch, sd, sync, cfg, theta[0], A[0], n[0], B, dev, peak)
+
     # ---- NEXT-3: host-offloaded outer state -- transfer cost of one fragment's A, v
     offload = None
     if world == 1 and not args.no_e2e:
@@ -483,6 +488,7 @@ def main():
             "m_sweep_emulated": m_sweep,
             "overlap": overlap,
             "offload": offload,
+            "inner_adamw_fused": fused,
         }
         print(json.dumps(line))
     sync.close()
@@ -570,6 +576,46 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
             "hidden": exposed <= 0.05 * tg, "inner_slowdown": to / ta if ta > 0 else None,
             "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,
                        "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0}}
+
+
+def fused_inner_run(torch, sd, sync, cfg, th, A0, n, B, dev, peak, reps=8):
+    """NEXT-1: AdamW inner step + quantize as two kernels (28 + 8.5 B/param)
+    vs the fused last-inner-step kernel (32.5 B/param: theta stays in
+    registers).  Fragment 0, libsd's k_adamw / k_quantize / k_adamw_quantize."""
+    import statistics as st
+
+    ctx = sync.ctx
+    g = torch.randn(n, device=dev) * 1e-3
+    m = torch.zeros(n, device=dev)
+    v = torch.zeros(n, device=dev)
+    mom = torch.zeros(n, device=dev)  # outer momentum (the merges only keep the calendar state legal)
+    hp = sd.SdAdamW(lr=3e-4, beta1=0.9, beta2=0.99, eps=1e-8, weight_decay=0.1)
+    slot = sync.slot(0)
+    t0 = cfg.H
+    sep, fus = [], []
+    for r in range(reps + 2):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record()
+        ctx.sd_inner_adamw(r + 1, th, g, m, v, hp, n)
+        ctx.sd_outer_grad_quantize(0, t0, th, A0, slot, n)
+        e[1].record()
+        ctx.sd_fragment_sync(0, t0, sync.gather[0], n)
+        ctx.sd_merge(0, t0 + cfg.tau, sync.gather[0], th, A0, mom, n)
+        e[2].record()
+        ctx.sd_inner_adamw_quantize(0, t0, r + 1, th, g, m, v, A0, slot, hp, n)
+        e[3].record()
+        ctx.sd_fragment_sync(0, t0, sync.gather[0], n)
+        ctx.sd_merge(0, t0 + cfg.tau, sync.gather[0], th, A0, mom, n)
+        torch.cuda.synchronize()
+        if r >= 2:
+            sep.append(e[0].elapsed_time(e[1]))
+            fus.append(e[2].elapsed_time(e[3]))
+    ts, tf = st.median(sep), st.median(fus)
+    pay = n / 2 + 4 * (1 if B == 0 else -(-n // B))
+    bs, bf = 36 * n + pay, 32 * n + pay
+    return {"fragment_elems": int(n), "separate_ms": ts, "fused_ms": tf, "speedup": ts / tf,
+            "separate_frac": bs / (ts / 1e3) / 1e9 / peak, "fused_frac": bf / (tf / 1e3) / 1e9 / peak,
+            "algorithmic_bytes_per_elem": {"separate": 36.5, "fused": 32.5}}
 
 
 def offload_run(torch, sync, A0, v0, n, P, dev, reps=5):

@@ -182,6 +182,28 @@ sd_status sd_state_writeback(sd_ctx* ctx, int32_t p, const float* anchor, const 
                              float* anchor_host, float* momentum_host, int64_t n, sd_stream stream);
 sd_status sd_state_sync(sd_ctx* ctx, sd_stream stream);
 
+/* InnerOpt = AdamW (NEXT-1; Alg. 2 L5; Adam as InnerOpt, P:77;
+ * SPEC.md:171-179 adamw_step with decoupled weight decay). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+} sd_adamw;
+
+/* One AdamW inner step (AdamW step index k >= 1, for the bias corrections):
+ *   m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2
+ *   theta = theta (1 - lr wd) - (lr / bc1) (m / (sqrt(v) / sqrt(bc2) + eps))
+ * bc_i = 1 - b_i^k evaluated in binary64 and rounded once; every other op
+ * rounds once (DESIGN.md AMB-20).  theta, m, v updated in place; grad read. */
+sd_status sd_inner_adamw(sd_ctx* ctx, int64_t k, float* theta, const float* grad, float* m, float* v, int64_t n,
+                         const sd_adamw* hp, sd_stream stream);
+
+/* The inner step that precedes a send, fused with Alg. 2 L7 + E3M0: same
+ * AdamW update, then fragment p's payload from the updated theta in the same
+ * pass (theta is not re-read), with sd_outer_grad_quantize's schedule and
+ * state rules (p sends at step t). */
+sd_status sd_inner_adamw_quantize(sd_ctx* ctx, int32_t p, int64_t t, int64_t k, float* theta, const float* grad,
+                                  float* m, float* v, const float* anchor, int64_t n, void* slot_out,
+                                  const sd_adamw* hp, sd_stream stream);
+
 /* Alg. 2 L7 + E3M0 (§8(a) a3).  p must be scheduled to send at t and not be
  * in flight.  Reads theta[n], anchor[n]; writes one payload
  * (sd_payload_bytes) at slot_out, which must be gather_buf + rank * payload

@@ -59,6 +59,7 @@ def lib():
             "or_apply": ([P, I32, I64, I32, F, F, F, P, P, P], ctypes.c_int),
             "or_round": ([I32, I64, I32, F, F, F, P, P, P, P, P], ctypes.c_int),
             "or_toy_run": ([C, I32, I64, ctypes.c_uint64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
+            "or_adamw": ([P, P, P, P, I64, I64, F, F, F, F, F], None),
             "or_toy_run_taus": ([C, I32, I64, ctypes.c_uint64, P, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -197,3 +198,8 @@ def toy_run_taus(c: OrConfig, M: int, block_len: int, seed: int, taus):
     bs = ctypes.c_int64(0)
     r = lib().or_toy_run_taus(ctypes.byref(c), M, block_len, seed, _p(t), _p(theta), _p(A), _p(v), ctypes.byref(bs))
     return theta, A, v, bs.value, r
+
+
+def adamw(theta, g, m, v, k, lr=1e-3, b1=0.9, b2=0.99, eps=1e-8, wd=0.0):
+    """One AdamW step in place on float32 arrays theta, m, v."""
+    lib().or_adamw(_p(theta), _p(g), _p(m), _p(v), theta.size, k, lr, b1, b2, eps, wd)

@@ -411,3 +411,31 @@ int or_toy_run_taus(const or_config* c, int32_t M, int64_t block_len, uint64_t s
   free(ev); free(nev); free(e); free(g); free(gather);
   return any_poison;
 }
+
+/* ===================================================================== */
+/* InnerOpt = AdamW (NEXT-1)                                             */
+/* ===================================================================== */
+
+/* One AdamW inner step (Alg. 2 L5; InnerOpt = Adam, P:77;
+ * SPEC.md:171-179 adamw_step, decoupled weight decay), step index k >= 1.
+ * Operation order (DESIGN.md §2 AMB-20), each op rounded once:
+ *   m <- b1*m + (1-b1)*g ;  v <- b2*v + (1-b2)*(g*g)
+ *   denom = sqrt(v) / sqrt(bc2) + eps
+ *   theta <- theta*(1 - lr*wd) - (lr/bc1) * (m / denom)
+ * with bc1 = 1 - b1^k, bc2 = 1 - b2^k (evaluated in binary64, rounded to
+ * binary32 once), and 1-b1, 1-b2, 1-lr*wd, lr/bc1, sqrt(bc2) rounded once. */
+void or_adamw(float* theta, const float* g, float* m, float* v, int64_t n, int64_t k, float lr, float b1,
+              float b2, float eps, float wd) {
+  const float bc1 = (float)(1.0 - pow((double)b1, (double)k));
+  const float bc2 = (float)(1.0 - pow((double)b2, (double)k));
+  const float c1 = 1.0f - b1, c2 = 1.0f - b2;
+  const float decay = 1.0f - lr * wd;
+  const float step = lr / bc1;
+  const float sbc2 = sqrtf(bc2);
+  for (int64_t i = 0; i < n; ++i) {
+    m[i] = b1 * m[i] + c1 * g[i];
+    v[i] = b2 * v[i] + c2 * (g[i] * g[i]);
+    const float denom = sqrtf(v[i]) / sbc2 + eps;
+    theta[i] = theta[i] * decay - step * (m[i] / denom);
+  }
+}

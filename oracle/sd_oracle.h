@@ -74,4 +74,8 @@ int or_toy_run(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, 
 int or_toy_run_taus(const or_config* c, int32_t M, int64_t block_len, uint64_t seed, const int32_t* taus,
                     float* theta, float* A_m, float* v_m, int64_t* bytes_sent);
 
+/* ---- InnerOpt = AdamW (NEXT-1) ---- */
+void or_adamw(float* theta, const float* g, float* m, float* v, int64_t n, int64_t k, float lr, float b1,
+              float b2, float eps, float wd);
+
 #endif /* SD_ORACLE_H_ */

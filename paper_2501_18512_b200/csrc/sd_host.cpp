@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -472,9 +473,12 @@ sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, floa
   return SD_OK;
 }
 
-sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor,
-                                 int64_t n, void* slot_out, sd_stream stream) {
-  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+namespace {
+
+// Checks shared by the two quantizing calls; on success the stream has waited
+// for a pending outer-state prefetch and the trailer's first_bad is reset.
+sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor, int64_t n,
+                     void* slot_out, cudaStream_t s, sdk::Payload* pl) {
   sd_status st;
   if ((st = check_fragment(c, p, t, n))) return st;
   if ((c->cfg.T == 0 || t <= c->cfg.T) ? !sends_at(&c->cfg, p, t) : true)
@@ -485,22 +489,100 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
                     (long long)c->fl[p].send_step);
   if ((st = check_ptr(c, slot_out, 256, "slot_out"))) return st;
   if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")))) return st;
-  const sdk::Payload pl = payload_of(&c->cfg, n);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  *pl = payload_of(&c->cfg, n);
   SD_CUDA(c, cudaSetDevice(c->device));
-  uint8_t* slot = static_cast<uint8_t*>(slot_out);
   if (c->prefetch_pending[p]) {  // offloaded outer state: the anchor must have landed
     SD_CUDA(c, cudaStreamWaitEvent(s, c->staged[p], 0));
     c->prefetch_pending[p] = 0;
   }
-  SD_CUDA(c, cudaMemsetAsync(slot + pl.trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64 - 1
-  const int k = sdk::launch_quantize(theta, anchor, pl, slot, c->num_sms, s);
-  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
-  g_launches += (uint64_t)k;
+  uint8_t* slot = static_cast<uint8_t*>(slot_out);
+  SD_CUDA(c, cudaMemsetAsync(slot + pl->trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64 - 1
+  return SD_OK;
+}
+
+void end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out) {
   c->fl[p].state = QUANTIZED;
   c->fl[p].send_step = t;
   c->fl[p].n = n;
   c->fl[p].slot = slot_out;
+}
+
+sd_status adam_hyper(sd_ctx* c, int64_t k, const sd_adamw* hp, sdk::AdamHyper* h) {
+  if (!hp) return ctx_fail(c, SD_ERR_ARG, "adamw hyper-parameter pointer is NULL");
+  if (k < 1) return ctx_fail(c, SD_ERR_ARG, "AdamW step k = %lld must be >= 1", (long long)k);
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f) || !(hp->beta2 >= 0.0f && hp->beta2 < 1.0f))
+    return ctx_fail(c, SD_ERR_CONFIG, "beta1 %g / beta2 %g not in [0, 1)", (double)hp->beta1, (double)hp->beta2);
+  if (!(hp->eps > 0.0f) || !(hp->lr == hp->lr) || !(hp->weight_decay == hp->weight_decay))
+    return ctx_fail(c, SD_ERR_CONFIG, "eps %g must be > 0, lr %g and weight_decay %g finite", (double)hp->eps,
+                    (double)hp->lr, (double)hp->weight_decay);
+  // constants of the op order (oracle or_adamw): bias corrections in binary64, rounded once
+  const float bc1 = (float)(1.0 - pow((double)hp->beta1, (double)k));
+  const float bc2 = (float)(1.0 - pow((double)hp->beta2, (double)k));
+  volatile float lw = hp->lr * hp->weight_decay;  // no contraction into 1 - lr*wd
+  h->b1 = hp->beta1;
+  h->b2 = hp->beta2;
+  h->c1 = 1.0f - hp->beta1;
+  h->c2 = 1.0f - hp->beta2;
+  h->decay = 1.0f - lw;
+  h->step = hp->lr / bc1;
+  h->sbc2 = sqrtf(bc2);
+  h->eps = hp->eps;
+  return SD_OK;
+}
+
+}  // namespace
+
+sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor,
+                                 int64_t n, void* slot_out, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  sdk::Payload pl;
+  sd_status st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl);
+  if (st != SD_OK) return st;
+  const int k = sdk::launch_quantize(theta, anchor, pl, static_cast<uint8_t*>(slot_out), c->num_sms, s);
+  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
+  g_launches += (uint64_t)k;
+  end_send(c, p, t, n, slot_out);
+  return SD_OK;
+}
+
+sd_status sd_inner_adamw(sd_ctx* c, int64_t k, float* theta, const float* grad, float* m, float* v, int64_t n,
+                         const sd_adamw* hp, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
+  sdk::AdamHyper h;
+  sd_status st = adam_hyper(c, k, hp, &h);
+  if (st != SD_OK) return st;
+  if (n == 0) return SD_OK;
+  if ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, grad, 32, "grad")) ||
+      (st = check_ptr(c, m, 32, "m")) || (st = check_ptr(c, v, 32, "v")))
+    return st;
+  SD_CUDA(c, cudaSetDevice(c->device));
+  const int kl = sdk::launch_adamw(theta, grad, m, v, n, h, c->num_sms, static_cast<cudaStream_t>(stream));
+  if (kl < 0) return cuda_fail(c, cudaGetLastError(), "k_adamw launch");
+  g_launches += (uint64_t)kl;
+  return SD_OK;
+}
+
+sd_status sd_inner_adamw_quantize(sd_ctx* c, int32_t p, int64_t t, int64_t k, float* theta, const float* grad,
+                                  float* m, float* v, const float* anchor, int64_t n, void* slot_out,
+                                  const sd_adamw* hp, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sdk::AdamHyper h;
+  sd_status st = adam_hyper(c, k, hp, &h);
+  if (st != SD_OK) return st;
+  if (n > 0 && ((st = check_ptr(c, grad, 32, "grad")) || (st = check_ptr(c, m, 32, "m")) ||
+                (st = check_ptr(c, v, 32, "v"))))
+    return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  sdk::Payload pl;
+  st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl);
+  if (st != SD_OK) return st;
+  const int kl = sdk::launch_adamw_quantize(theta, grad, m, v, anchor, pl, static_cast<uint8_t*>(slot_out), h,
+                                            c->num_sms, s);
+  if (kl < 0) return cuda_fail(c, cudaGetLastError(), "k_adamw_quantize launch");
+  g_launches += (uint64_t)kl;
+  end_send(c, p, t, n, slot_out);
   return SD_OK;
 }
 

@@ -248,11 +248,10 @@ __device__ void write_tail(const QArgs& a) {
 // k_quantize: single pass, B in {256, 512, 1024} (NB = 1024 / B blocks per
 // warp chunk).  One warp per 1024-element chunk, grid-stride over chunks.
 // ---------------------------------------------------------------------------
+// Block maxima, poison check, codes and scales of a chunk whose Deltas are in d.
 template <int NB, bool kFullChunk>
-__device__ __forceinline__ void quantize_chunk(const QArgs& a, int64_t c, int lane) {
+__device__ __forceinline__ void encode_block_rows(const QArgs& a, int64_t c, int lane, const f8 (&d)[4]) {
   constexpr int KB = 4 / NB;  // rows per scale block
-  f8 d[4];
-  load_chunk<kFullChunk>(a, c, lane, d);
   float s[NB];
   bool bad = false;
 #pragma unroll
@@ -273,6 +272,13 @@ __device__ __forceinline__ void quantize_chunk(const QArgs& a, int64_t c, int la
     for (int q = 1; q < NB; ++q) sv = (lane == q) ? s[q] : sv;
     if (blk < a.nb) reinterpret_cast<float*>(a.slot + a.scales_off)[blk] = sv;
   }
+}
+
+template <int NB, bool kFullChunk>
+__device__ __forceinline__ void quantize_chunk(const QArgs& a, int64_t c, int lane) {
+  f8 d[4];
+  load_chunk<kFullChunk>(a, c, lane, d);
+  encode_block_rows<NB, kFullChunk>(a, c, lane, d);
 }
 
 template <int NB>
@@ -362,6 +368,107 @@ __global__ void __launch_bounds__(kThreads) k_encode(QArgs a) {
   const int64_t nfull = a.n >> 10;
   for (int64_t c = warp; c < nfull; c += nwarps) encode_chunk<true>(a, c, lane);
   if ((nfull << 10) < a.n && warp == nfull % nwarps) encode_chunk<false>(a, nfull, lane);
+  if (blockIdx.x == 0) write_tail(a);
+}
+
+// ---------------------------------------------------------------------------
+// InnerOpt = AdamW (NEXT-1; Alg. 2 L5), with
+// the op order of the oracle's or_adamw (DESIGN.md AMB-20):
+//   m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2
+//   theta = theta (1 - lr wd) - (lr/bc1) (m / (sqrt(v)/sqrt(bc2) + eps))
+// k_adamw: one thread per 8 elements (256-bit accesses).  k_adamw_quantize:
+// the inner step that precedes a send, fused with Alg. 2 L7 + E3M0 -- the
+// updated theta stays in registers, so the quantize costs 4.5 B/param of
+// extra traffic (A read + codes) instead of 8.5.
+// ---------------------------------------------------------------------------
+struct AdamArgs {
+  float* theta;
+  const float* grad;
+  float* m;
+  float* v;
+  int64_t n;
+  float b1, b2, c1, c2, decay, step, sbc2, eps;
+};
+
+__device__ __forceinline__ void adamw_one(float& th, float g, float& m, float& v, const AdamArgs& h) {
+  m = __fadd_rn(__fmul_rn(h.b1, m), __fmul_rn(h.c1, g));
+  v = __fadd_rn(__fmul_rn(h.b2, v), __fmul_rn(h.c2, __fmul_rn(g, g)));
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), h.sbc2), h.eps);
+  th = __fsub_rn(__fmul_rn(th, h.decay), __fmul_rn(h.step, __fdiv_rn(m, denom)));
+}
+
+__global__ void __launch_bounds__(kThreads) k_adamw(AdamArgs h) {
+  const int64_t n8 = h.n >> 3;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += nthr) {
+    f8 t = ld8(h.theta + 8 * i), g = ld8_stream(h.grad + 8 * i), m = ld8(h.m + 8 * i), v = ld8(h.v + 8 * i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) adamw_one(t.v[j], g.v[j], m.v[j], v.v[j], h);
+    st8(h.theta + 8 * i, t);
+    st8(h.m + 8 * i, m);
+    st8(h.v + 8 * i, v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (h.n & 7)) {
+    const int64_t e = (n8 << 3) + threadIdx.x;
+    float t = h.theta[e], m = h.m[e], v = h.v[e];
+    adamw_one(t, h.grad[e], m, v, h);
+    h.theta[e] = t;
+    h.m[e] = m;
+    h.v[e] = v;
+  }
+}
+
+// AdamW on the chunk's 4 rows, write back theta, m, v; d = A - theta'.
+template <bool kFullChunk>
+__device__ __forceinline__ void adamw_chunk(const QArgs& a, const AdamArgs& h, int64_t c, int lane, f8 (&d)[4]) {
+  const int64_t e0 = c * 1024 + 8 * lane;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t e = e0 + 256 * k;
+    if (kFullChunk) {
+      f8 t = ld8(h.theta + e), g = ld8_stream(h.grad + e), m = ld8(h.m + e), v = ld8(h.v + e);
+      const f8 an = ld8_stream(a.anchor + e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        adamw_one(t.v[j], g.v[j], m.v[j], v.v[j], h);
+        d[k].v[j] = __fsub_rn(an.v[j], t.v[j]);  // Alg. 2 L7 on the updated theta
+      }
+      st8(h.theta + e, t);
+      st8(h.m + e, m);
+      st8(h.v + e, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        d[k].v[j] = 0.0f;
+        if (e + j < a.n) {
+          float t = h.theta[e + j], m = h.m[e + j], v = h.v[e + j];
+          adamw_one(t, h.grad[e + j], m, v, h);
+          h.theta[e + j] = t;
+          h.m[e + j] = m;
+          h.v[e + j] = v;
+          d[k].v[j] = __fsub_rn(a.anchor[e + j], t);
+        }
+      }
+    }
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads) k_adamw_quantize(QArgs a, AdamArgs h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nfull = a.n >> 10;
+  for (int64_t c = warp; c < nfull; c += nwarps) {
+    f8 d[4];
+    adamw_chunk<true>(a, h, c, lane, d);
+    encode_block_rows<NB, true>(a, c, lane, d);
+  }
+  if ((nfull << 10) < a.n && warp == nfull % nwarps) {
+    f8 d[4];
+    adamw_chunk<false>(a, h, nfull, lane, d);
+    encode_block_rows<NB, false>(a, nfull, lane, d);
+  }
   if (blockIdx.x == 0) write_tail(a);
 }
 
@@ -543,6 +650,64 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
     launched = 2;
   }
   return cudaGetLastError() == cudaSuccess ? launched : -1;
+}
+
+namespace {
+AdamArgs make_adam(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamHyper& hp) {
+  AdamArgs h;
+  h.theta = theta;
+  h.grad = grad;
+  h.m = m;
+  h.v = v;
+  h.n = n;
+  h.b1 = hp.b1;
+  h.b2 = hp.b2;
+  h.c1 = hp.c1;
+  h.c2 = hp.c2;
+  h.decay = hp.decay;
+  h.step = hp.step;
+  h.sbc2 = hp.sbc2;
+  h.eps = hp.eps;
+  return h;
+}
+}  // namespace
+
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamHyper& hp, int num_sms,
+                 cudaStream_t st) {
+  const AdamArgs h = make_adam(theta, grad, m, v, n, hp);
+  const int64_t items = (n >> 3) > 0 ? (n >> 3) : 1;
+  k_adamw<<<grid_for(k_adamw, num_sms, items, kThreads), kThreads, 0, st>>>(h);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
+                          uint8_t* slot, const AdamHyper& hp, int num_sms, cudaStream_t st) {
+  if (!(pl.B == 256 || pl.B == 512 || pl.B == 1024)) {  // two-pass scales: AdamW, then quantize
+    const int k1 = launch_adamw(theta, grad, m, v, pl.n, hp, num_sms, st);
+    if (k1 < 0) return -1;
+    const int k2 = launch_quantize(theta, anchor, pl, slot, num_sms, st);
+    return k2 < 0 ? -1 : k1 + k2;
+  }
+  QArgs a;
+  a.theta = theta;
+  a.anchor = anchor;
+  a.n = pl.n;
+  a.nb = pl.nb;
+  a.lgB = ilog2_or_neg(pl.B);
+  a.slot = slot;
+  a.scales_off = pl.scales_off;
+  a.trailer_off = pl.trailer_off;
+  a.bytes = pl.bytes;
+  const AdamArgs h = make_adam(theta, grad, m, v, pl.n, hp);
+  const int64_t chunks = (pl.n + 1023) >> 10;
+  const int wpb = kThreads / 32;
+  if (pl.B == 1024)
+    k_adamw_quantize<1><<<grid_for(k_adamw_quantize<1>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
+  else if (pl.B == 512)
+    k_adamw_quantize<2><<<grid_for(k_adamw_quantize<2>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
+  else
+    k_adamw_quantize<4><<<grid_for(k_adamw_quantize<4>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor, float* momentum,

@@ -21,6 +21,25 @@ struct Payload {          // byte offsets inside one replica payload (sd.h)
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot,
                     int num_sms, cudaStream_t st);
 
+// AdamW hyper-parameters with the host-side constants of the op order
+// (bias corrections in binary64 rounded once, DESIGN.md AMB-20).
+struct AdamHyper {
+  float b1, b2, c1, c2;  // beta1, beta2, 1 - beta1, 1 - beta2
+  float decay;           // 1 - lr * wd
+  float step;            // lr / bc1
+  float sbc2;            // sqrt(bc2)
+  float eps;
+};
+
+// One AdamW inner step over n elements (theta, m, v in place).
+int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n, const AdamHyper& hp, int num_sms,
+                 cudaStream_t st);
+
+// AdamW step fused with Delta + E3M0 of the updated theta into one payload
+// (single pass for B in {256, 512, 1024}; AdamW + two-pass quantize otherwise).
+int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
+                          uint8_t* slot, const AdamHyper& hp, int num_sms, cudaStream_t st);
+
 // Fused decode + M-way fp32 mean + Nesterov + anchor update + alpha-merge.
 // status: host-mapped pinned word pair {first_bad, flags} written when the
 // round is skipped.  Returns kernels launched or -1.

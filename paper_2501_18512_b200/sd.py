@@ -28,7 +28,7 @@ EXPORTS = (
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free",
     "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync",
-    "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
+    "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
 
@@ -40,6 +40,11 @@ class SdConfig(ctypes.Structure):
         ("tau", ctypes.c_int32), ("T", ctypes.c_int64), ("alpha", ctypes.c_float), ("outer_lr", ctypes.c_float),
         ("outer_momentum", ctypes.c_float), ("scale_block", ctypes.c_int32),
     ]
+
+
+class SdAdamW(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
+                ("weight_decay", ctypes.c_float)]
 
 
 class SdError(RuntimeError):
@@ -81,6 +86,8 @@ def lib():
             "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_sync": ([P, P], I32),
             "sd_outer_grad_quantize": ([P, I32, I64, P, P, I64, P, P], I32),
+            "sd_inner_adamw": ([P, I64, P, P, P, P, I64, ctypes.POINTER(SdAdamW), P], I32),
+            "sd_inner_adamw_quantize": ([P, I32, I64, I64, P, P, P, P, P, I64, P, ctypes.POINTER(SdAdamW), P], I32),
             "sd_fragment_sync": ([P, I32, I64, P, I64, P], I32),
             "sd_fragment_wait": ([P, I32, I64, P], I32),
             "sd_merge": ([P, I32, I64, P, P, P, P, I64, P], I32),
@@ -253,6 +260,16 @@ class SdContext:
     def sd_outer_grad_quantize(self, p, t, theta, anchor, slot_out, n=None, stream=None):
         n = theta.numel() if n is None else n
         self._c(lib().sd_outer_grad_quantize(self.h, p, t, _ptr(theta), _ptr(anchor), n, _ptr(slot_out), _stream(stream)))
+
+    def sd_inner_adamw(self, k, theta, grad, m, v, hp: SdAdamW, n=None, stream=None):
+        n = theta.numel() if n is None else n
+        self._c(lib().sd_inner_adamw(self.h, k, _ptr(theta), _ptr(grad), _ptr(m), _ptr(v), n, ctypes.byref(hp),
+                                     _stream(stream)))
+
+    def sd_inner_adamw_quantize(self, p, t, k, theta, grad, m, v, anchor, slot_out, hp: SdAdamW, n=None, stream=None):
+        n = theta.numel() if n is None else n
+        self._c(lib().sd_inner_adamw_quantize(self.h, p, t, k, _ptr(theta), _ptr(grad), _ptr(m), _ptr(v),
+                                              _ptr(anchor), n, _ptr(slot_out), ctypes.byref(hp), _stream(stream)))
 
     def sd_fragment_sync(self, p, t, gather_buf, n, stream=None):
         self._c(lib().sd_fragment_sync(self.h, p, t, _ptr(gather_buf), n, _stream(stream)))

@@ -423,3 +423,54 @@ def test_offloaded_outer_state_toy_run():
         assert_same(torch.cat(v_h[m]), v_o, f"host momentum store replica {m}")
     for c in ctx:
         c.sd_finalize()
+
+
+# ------------------------------------------------------------ InnerOpt (NEXT-1)
+HP = dict(lr=3e-4, beta1=0.9, beta2=0.99, eps=1e-8, weight_decay=0.1)
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 8 * 1024 + 5, 300001])
+def test_inner_adamw_bit_exact(n):
+    rng = np.random.default_rng(n)
+    th = rng.standard_normal(n).astype(np.float32) * 0.02
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    ctx = sd.SdContext(cfg_for(1024), 0, 1, None, 0)
+    hp = sd.SdAdamW(**HP)
+    th_d, m_d, v_d = to_dev(th), to_dev(m), to_dev(v)
+    for k in range(1, 4):
+        g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+        g[:: 97] = 0.0
+        ctx.sd_inner_adamw(k, th_d, to_dev(g), m_d, v_d, hp, n)
+        oracle.adamw(th, g, m, v, k, lr=HP["lr"], b1=HP["beta1"], b2=HP["beta2"], eps=HP["eps"], wd=HP["weight_decay"])
+    torch.cuda.synchronize()
+    assert_same(th_d, th, "theta")
+    assert_same(m_d, m, "m")
+    assert_same(v_d, v, "v")
+    ctx.sd_finalize()
+
+
+@pytest.mark.parametrize("B", [1024, 256, 0])
+@pytest.mark.parametrize("n", [1025, 64 * 1024 + 77])
+def test_inner_adamw_quantize_fused_bit_exact(n, B):
+    """The fused last-inner-step + quantize equals AdamW then or_quantize."""
+    rng = np.random.default_rng(n + B)
+    A = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    th = (A - rng.standard_normal(n).astype(np.float32) * 1e-3).astype(np.float32)
+    m = (rng.standard_normal(n) * 1e-4).astype(np.float32)
+    v = (rng.random(n) * 1e-7).astype(np.float32)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    cfg = cfg_for(B)
+    rep = EmulatedReplicas(cfg, 1, n)
+    hp = sd.SdAdamW(**HP)
+    th_d, m_d, v_d = to_dev(th), to_dev(m), to_dev(v)
+    rep.ctx[0].sd_inner_adamw_quantize(0, 10, 7, th_d, to_dev(g), m_d, v_d, to_dev(A), rep.slot(0), hp, n)
+    torch.cuda.synchronize()
+    oracle.adamw(th, g, m, v, 7, lr=HP["lr"], b1=HP["beta1"], b2=HP["beta2"], eps=HP["eps"], wd=HP["weight_decay"])
+    want, _ = oracle.quantize(th, A, B)
+    assert np.array_equal(rep.gather.cpu().numpy(), want)
+    assert_same(th_d, th, "theta")
+    assert_same(m_d, m, "m")
+    assert_same(v_d, v, "v")
+    rep.ctx[0].sd_fragment_sync(0, 10, rep.gather, n)
+    rep.close()

@@ -276,3 +276,41 @@ def test_per_replica_tau_slack_keeps_outer_state_replicated():
     assert np.array_equal(bits(A[0]), bits(A[1])) and np.array_equal(bits(v[0]), bits(v[1]))
     th_eq, A_eq, _, _, _ = oracle.toy_run(c, 2, 2048, 11)
     assert not np.array_equal(bits(th[1]), bits(th_eq[1]))
+
+
+# --------------------------------------------------------------- InnerOpt (NEXT-1)
+def test_adamw_spec_examples():
+    """SPEC.md:177-179 adamw_step examples."""
+    th = np.array([0.3, -1.25], np.float32)
+    m, v = np.zeros(2, np.float32), np.zeros(2, np.float32)
+    oracle.adamw(th, np.zeros(2, np.float32), m, v, 1, lr=0.1, wd=0.0)       # g = 0 -> unchanged
+    assert th.tolist() == [np.float32(0.3), -1.25]
+    th = np.zeros(1, np.float32)
+    m, v = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    oracle.adamw(th, np.array([0.5], np.float32), m, v, 1, lr=0.1, wd=0.0)   # first step -> ~ -lr
+    assert abs(th[0] + 0.1) < 1e-6
+    th = np.ones(1, np.float32)
+    m, v = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    oracle.adamw(th, np.zeros(1, np.float32), m, v, 1, lr=0.1, wd=0.1)      # decoupled decay only -> 0.99
+    assert th[0] == np.float32(0.99)
+
+
+def test_adamw_vs_torch():
+    """torch.optim.AdamW (betas, eps, decoupled weight decay) over 5 steps from
+    the same state; torch computes exp_avg by lerp and may contract, so the
+    comparison is operand-scaled (moments and parameters)."""
+    rng = np.random.default_rng(2)
+    n = 50000
+    th = rng.standard_normal(n).astype(np.float32)
+    m, v = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    p = torch.nn.Parameter(torch.from_numpy(th.copy()))
+    opt = torch.optim.AdamW([p], lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=0.1)
+    for k in range(1, 6):
+        g = (rng.standard_normal(n) * 0.01).astype(np.float32)
+        p.grad = torch.from_numpy(g.copy())
+        opt.step()
+        oracle.adamw(th, g, m, v, k, lr=1e-3, b1=0.9, b2=0.99, eps=1e-8, wd=0.1)
+        st = opt.state[p]
+        assert np.allclose(st["exp_avg"].numpy(), m, rtol=1e-5, atol=1e-9)
+        assert np.allclose(st["exp_avg_sq"].numpy(), v, rtol=1e-5, atol=1e-12)
+        assert np.max(np.abs(p.detach().numpy() - th)) <= 1e-6 * max(1.0, float(np.max(np.abs(th))))
