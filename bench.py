@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-m-sweep", action="store_true")
     ap.add_argument("--serial", action="store_true", help="no send/receive pipelining across fragments")
+    ap.add_argument("--gather", choices=["auto", "ce", "push"], default="auto",
+                    help="all-gather: NCCL copy engines (ce), fused into the quantize kernel (push), "
+                         "or libsd's choice (auto: push iff tau == 0)")
     return ap.parse_args()
 
 
@@ -145,6 +148,7 @@ def workload_config(wl, B, world):
     return {"workload": wl.describe() + f"; M = {world} replica(s), one per GPU; E3M0 B={B}",
             "fragments": None, "l2": "inputs > L2 (fragments of 0.6-0.9 GB per fp32 array, cycled); no flush",
             "parallelism": f"diloco-replicas{world}"}
+
 
 
 # --------------------------------------------------------------------------- oracle timing
@@ -259,7 +263,9 @@ def main():
         th = A[p].clone()
         synth.dev_apply_window(th, segs[p], p, rank, 1)
         theta.append(th)
-    sync = FragmentSync(cfg, n, rank, world, local)
+    sync = FragmentSync(cfg, n, rank, world, local,
+                        gather_mode={"auto": sd.SD_GATHER_AUTO, "ce": sd.SD_GATHER_COPY_ENGINE,
+                                     "push": sd.SD_GATHER_PUSH}[args.gather])
     torch.cuda.synchronize()
 
     K, W = args.steps, max(1, args.warmup)
@@ -461,6 +467,10 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
             "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n],
+                           gather=("fused into k_quantize: NVLink stores to the peers' symmetric buffers + "
+                                   "flag handshake" if (args.gather == "push" or
+                                                        (args.gather == "auto" and cfg.tau == 0)) else
+                                   "NCCL in-place all-gather on copy engines (symmetric window, zero CTAs)"),
                            l2=("state (12 B/param) fits in ~4x L2: L2 flushed (2x L2 written) between steps, "
                                "only the steps are timed" if flush else
                                "inputs > L2 (fragments of %.0f-%.0f MB per fp32 array, cycled); no flush"

@@ -157,6 +157,28 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
 sd_status sd_gather_alloc(sd_ctx* ctx, int64_t n, void** out);
 sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
 
+/* How the all-gather of Alg. 2 L8 is carried out for buffers from
+ * sd_gather_alloc (set before allocating; default SD_GATHER_AUTO):
+ *  SD_GATHER_COPY_ENGINE  sd_fragment_sync issues NCCL's in-place all-gather
+ *                         on the comm stream (copy engines, zero SMs); it
+ *                         overlaps whatever the compute stream does next.
+ *  SD_GATHER_PUSH         fused: the quantize kernel stores every payload
+ *                         word into this rank's slot of each peer's buffer
+ *                         over NVLink as it produces it (NCCL symmetric-window
+ *                         LSA pointers), then release-signals a per-round
+ *                         flag; the block-receive is an acquire-wait on the
+ *                         peers' flags.  Buffers hold two rounds (alternating
+ *                         by send index), so no rendezvous is needed.
+ * With caller-owned buffers or without a communicator the mode is ignored. */
+#define SD_GATHER_COPY_ENGINE 0
+#define SD_GATHER_PUSH 1
+#define SD_GATHER_AUTO 2 /* default: PUSH when tau == 0 (nothing to overlap the gather with), else COPY_ENGINE */
+sd_status sd_set_gather_mode(sd_ctx* ctx, int32_t mode);
+
+/* Address of the M payloads of fragment p's round sent at step t inside
+ * gather_buf (the buffer itself, or its round-parity half in push mode). */
+sd_status sd_gather_payloads(sd_ctx* ctx, int32_t p, int64_t t, const void* gather_buf, const void** out);
+
 /* Outer-state store init (§8(a) a2; AMB-2): anchor <- theta, momentum <- 0. */
 sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, float* momentum,
                               int64_t n, sd_stream stream);

@@ -122,6 +122,9 @@ struct Inflight {
   int64_t n = 0;
   const void* slot = nullptr;
   const void* gather = nullptr;
+  bool push = false;      // payloads were pushed by the quantize (fused all-gather)
+  bool waited = false;    // push mode: the block-receive wait kernel was issued
+  size_t half_off = 0;    // push mode: byte offset of this round's half
 };
 
 }  // namespace
@@ -131,11 +134,15 @@ struct GatherBuf {
   size_t bytes = 0;
   ncclWindow_t win = nullptr;
   bool nccl = false;
+  bool push = false;   // fused-push layout: two halves (round parity) of M payloads + M round flags
+  size_t half = 0;     // bytes per half
+  size_t pb = 0;       // payload bytes
 };
 
 struct sd_ctx {
   sd_config cfg;
   std::vector<GatherBuf> bufs;
+  int32_t gather_mode = SD_GATHER_AUTO;
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -151,6 +158,14 @@ struct sd_ctx {
 };
 
 namespace {
+
+GatherBuf* find_buf(sd_ctx* c, const void* p) {
+  for (GatherBuf& b : c->bufs)
+    if (static_cast<const char*>(p) >= static_cast<const char*>(b.ptr) &&
+        static_cast<const char*>(p) < static_cast<const char*>(b.ptr) + b.bytes)
+      return &b;
+  return nullptr;
+}
 
 sd_status cuda_fail(sd_ctx* c, cudaError_t e, const char* what) {
   snprintf(g_err, sizeof g_err, "%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
@@ -364,7 +379,16 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   if (n < 0) return ctx_fail(c, SD_ERR_ARG, "n = %lld is negative", (long long)n);
   SD_CUDA(c, cudaSetDevice(c->device));
   GatherBuf b;
-  b.bytes = (size_t)align_up((int64_t)(payload_of(&c->cfg, n).bytes * (size_t)c->M), 2 << 20);
+  b.pb = payload_of(&c->cfg, n).bytes;
+  // measured on B200: the fused push wins when the gather is on the
+  // critical path (tau = 0); with tau >= 1 the copy-engine gather is hidden
+  b.push = c->comm && (c->gather_mode == SD_GATHER_PUSH || (c->gather_mode == SD_GATHER_AUTO && c->cfg.tau == 0));
+  if (b.push) {
+    b.half = (size_t)align_up((int64_t)(b.pb * (size_t)c->M) + 256, 256);
+    b.bytes = (size_t)align_up((int64_t)(2 * b.half), 2 << 20);
+  } else {
+    b.bytes = (size_t)align_up((int64_t)(b.pb * (size_t)c->M), 2 << 20);
+  }
   if (c->comm) {
     ncclResult_t r = ncclMemAlloc(&b.ptr, b.bytes);
     if (r != ncclSuccess) return ctx_fail(c, SD_ERR_NCCL, "ncclMemAlloc(%zu): %s", b.bytes, ncclGetErrorString(r));
@@ -377,8 +401,36 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   } else {
     SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
   }
+  if (b.push) {  // round flags start at 0 (never a send step)
+    SD_CUDA(c, cudaMemset(b.ptr, 0, b.bytes));
+    SD_CUDA(c, cudaDeviceSynchronize());
+  }
   c->bufs.push_back(b);
   *out = b.ptr;
+  return SD_OK;
+}
+
+sd_status sd_gather_payloads(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, const void** out) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (!out) return ctx_fail(c, SD_ERR_ARG, "out pointer is NULL");
+  if (p < 0 || p >= c->P) return ctx_fail(c, SD_ERR_ARG, "fragment %d out of range [0, %d)", p, c->P);
+  *out = gather_buf;
+  GatherBuf* b = find_buf(c, gather_buf);
+  if (b && b->push) {
+    const int64_t round = (t - offset_of(&c->cfg, p)) / c->cfg.H;
+    *out = static_cast<const char*>(b->ptr) + (size_t)(round & 1) * b->half;
+  }
+  return SD_OK;
+}
+
+sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO)
+    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH or SD_GATHER_AUTO",
+                    mode);
+  for (const Inflight& f : c->fl)
+    if (f.state != IDLE) return ctx_fail(c, SD_ERR_STATE, "gather mode changed while a fragment is in flight");
+  c->gather_mode = mode;
   return SD_OK;
 }
 
@@ -475,10 +527,38 @@ sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, floa
 
 namespace {
 
+// Push mode: where this round's payloads live and the push spec of the quantize.
+struct PushRound {
+  GatherBuf* buf = nullptr;
+  size_t half_off = 0;
+  sdk::Push push;
+};
+
+sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk::Payload& pl, PushRound* r) {
+  GatherBuf* b = find_buf(c, slot_out);
+  if (!b || !b->push) return SD_OK;
+  if (b->pb != pl.bytes) return ctx_fail(c, SD_ERR_ARG, "gather buffer was allocated for payloads of %zu bytes, not %zu", b->pb, pl.bytes);
+  if (static_cast<char*>(slot_out) != static_cast<char*>(b->ptr) + (size_t)c->rank * pl.bytes)
+    return ctx_fail(c, SD_ERR_ARG, "slot_out must be gather_buf + rank * payload");
+  const int64_t round = (t - offset_of(&c->cfg, p)) / c->cfg.H;  // send index of fragment p
+  r->buf = b;
+  r->half_off = (size_t)(round & 1) * b->half;
+  r->push.win = b->win;
+  r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
+  r->push.rank = c->rank;
+  r->push.M = c->M;
+  return SD_OK;
+}
+
 // Checks shared by the two quantizing calls; on success the stream has waited
 // for a pending outer-state prefetch and the trailer's first_bad is reset.
+uint8_t* local_slot(sd_ctx* c, void* slot_out, const PushRound& pr, const sdk::Payload& pl) {
+  if (!pr.buf) return static_cast<uint8_t*>(slot_out);
+  return static_cast<uint8_t*>(pr.buf->ptr) + pr.half_off + (size_t)c->rank * pl.bytes;
+}
+
 sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor, int64_t n,
-                     void* slot_out, cudaStream_t s, sdk::Payload* pl) {
+                     void* slot_out, cudaStream_t s, sdk::Payload* pl, PushRound* pr) {
   sd_status st;
   if ((st = check_fragment(c, p, t, n))) return st;
   if ((c->cfg.T == 0 || t <= c->cfg.T) ? !sends_at(&c->cfg, p, t) : true)
@@ -490,21 +570,32 @@ sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const 
   if ((st = check_ptr(c, slot_out, 256, "slot_out"))) return st;
   if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")))) return st;
   *pl = payload_of(&c->cfg, n);
+  if ((st = push_round(c, p, t, slot_out, *pl, pr))) return st;
   SD_CUDA(c, cudaSetDevice(c->device));
   if (c->prefetch_pending[p]) {  // offloaded outer state: the anchor must have landed
     SD_CUDA(c, cudaStreamWaitEvent(s, c->staged[p], 0));
     c->prefetch_pending[p] = 0;
   }
-  uint8_t* slot = static_cast<uint8_t*>(slot_out);
-  SD_CUDA(c, cudaMemsetAsync(slot + pl->trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64 - 1
+  SD_CUDA(c, cudaMemsetAsync(local_slot(c, slot_out, *pr, *pl) + pl->trailer_off + 8, 0xFF, 8, s));  // first_bad = 2^64-1
   return SD_OK;
 }
 
-void end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out) {
+sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, const PushRound& pr,
+                   const sdk::Payload& pl, cudaStream_t s) {
+  if (pr.buf) {  // fused all-gather: publish this round to the peers
+    const int k = sdk::launch_push_signal(pl, local_slot(c, slot_out, pr, pl), pr.push,
+                                          pr.half_off + (size_t)c->M * pl.bytes, (uint64_t)t, s);
+    if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_signal launch");
+    g_launches += (uint64_t)k;
+  }
   c->fl[p].state = QUANTIZED;
   c->fl[p].send_step = t;
   c->fl[p].n = n;
   c->fl[p].slot = slot_out;
+  c->fl[p].push = pr.buf != nullptr;
+  c->fl[p].waited = false;
+  c->fl[p].half_off = pr.half_off;
+  return SD_OK;
 }
 
 sd_status adam_hyper(sd_ctx* c, int64_t k, const sd_adamw* hp, sdk::AdamHyper* h) {
@@ -537,13 +628,13 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   sdk::Payload pl;
-  sd_status st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl);
+  PushRound pr;
+  sd_status st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
-  const int k = sdk::launch_quantize(theta, anchor, pl, static_cast<uint8_t*>(slot_out), c->num_sms, s);
+  const int k = sdk::launch_quantize(theta, anchor, pl, local_slot(c, slot_out, pr, pl), pr.push, c->num_sms, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
   g_launches += (uint64_t)k;
-  end_send(c, p, t, n, slot_out);
-  return SD_OK;
+  return end_send(c, p, t, n, slot_out, pr, pl, s);
 }
 
 sd_status sd_inner_adamw(sd_ctx* c, int64_t k, float* theta, const float* grad, float* m, float* v, int64_t n,
@@ -576,14 +667,14 @@ sd_status sd_inner_adamw_quantize(sd_ctx* c, int32_t p, int64_t t, int64_t k, fl
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   sdk::Payload pl;
-  st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl);
+  PushRound pr;
+  st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
-  const int kl = sdk::launch_adamw_quantize(theta, grad, m, v, anchor, pl, static_cast<uint8_t*>(slot_out), h,
-                                            c->num_sms, s);
+  const int kl = sdk::launch_adamw_quantize(theta, grad, m, v, anchor, pl, local_slot(c, slot_out, pr, pl), h,
+                                            pr.push, c->num_sms, s);
   if (kl < 0) return cuda_fail(c, cudaGetLastError(), "k_adamw_quantize launch");
   g_launches += (uint64_t)kl;
-  end_send(c, p, t, n, slot_out);
-  return SD_OK;
+  return end_send(c, p, t, n, slot_out, pr, pl, s);
 }
 
 sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, int64_t n, sd_stream stream) {
@@ -602,7 +693,9 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
                     c->rank, pl.bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
-  if (c->comm) {
+  if (f.push) {  // the payloads were pushed by the quantize: nothing to transfer
+    SD_CUDA(c, cudaEventRecord(c->done[p], s));
+  } else if (c->comm) {
     SD_CUDA(c, cudaEventRecord(c->ready[p], s));
     SD_CUDA(c, cudaStreamWaitEvent(c->comm_stream, c->ready[p], 0));
     ncclResult_t r = ncclAllGather(g + (size_t)c->rank * pl.bytes, g, pl.bytes, ncclUint8, c->comm, c->comm_stream);
@@ -615,6 +708,25 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
   f.gather = gather_buf;
   return SD_OK;
 }
+
+namespace {
+// push mode block-receive: one wait kernel per round (30 s bound per peer)
+sd_status issue_push_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
+  Inflight& f = c->fl[p];
+  if (!f.push || f.waited) return SD_OK;
+  GatherBuf* b = find_buf(c, f.gather);
+  if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: push-mode gather buffer not found", p);
+  const sdk::Payload pl = payload_of(&c->cfg, f.n);
+  uint8_t* half = static_cast<uint8_t*>(b->ptr) + f.half_off;
+  const int k = sdk::launch_push_wait(reinterpret_cast<const unsigned long long*>(half + (size_t)c->M * pl.bytes),
+                                      half, pl, c->M, c->rank, (uint64_t)f.send_step, 30ull * 1000000000ull,
+                                      c->status_dev, s);
+  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_wait launch");
+  g_launches += (uint64_t)k;
+  f.waited = true;
+  return SD_OK;
+}
+}  // namespace
 
 sd_status sd_fragment_wait(sd_ctx* c, int32_t p, int64_t t, sd_stream stream) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
@@ -629,7 +741,7 @@ sd_status sd_fragment_wait(sd_ctx* c, int32_t p, int64_t t, sd_stream stream) {
                     (long long)t, (long long)s_step);
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->done[p], 0));
-  return SD_OK;
+  return issue_push_wait(c, p, static_cast<cudaStream_t>(stream));
 }
 
 sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
@@ -655,7 +767,9 @@ sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
-  const int k = sdk::launch_apply(static_cast<const uint8_t*>(gather_buf), pl, c->M, theta, anchor, momentum,
+  if ((st = issue_push_wait(c, p, s))) return st;
+  const uint8_t* payloads = static_cast<const uint8_t*>(gather_buf) + (f.push ? f.half_off : 0);
+  const int k = sdk::launch_apply(payloads, pl, c->M, theta, anchor, momentum,
                                   c->cfg.outer_lr, c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_apply launch");
   g_launches += (uint64_t)k;

@@ -26,6 +26,8 @@
 //   e = max(0, 7 - ((bits(T_0) + 2^23 - 1 - bits(|d|)) >> 23)).
 // Blocks whose T_6 would be subnormal (s < ~2^-119.5) take the 7-compare path.
 #include <cuda_runtime.h>
+#include <nccl.h>
+#include <nccl_device.h>
 #include <float.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -75,6 +77,12 @@ __device__ __forceinline__ uint32_t ld_code_word(const uint32_t* p) {
 
 __device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Smallest binary32 x >= 0 with (double)x * x >= s^2 * 2^(-2j-1): |d| >= T_j
 // <=> d^2 >= s^2 2^(-2j-1) exactly, i.e. |d|/s >= 2^(-j-1/2), the log2
 // midpoint between grid points 2^-j and 2^-(j+1).  s = 0 -> +inf (all codes 0).
@@ -122,7 +130,23 @@ struct QArgs {
   int32_t lgB;      // log2(B), or -1 for one block per fragment
   uint8_t* slot;    // payload base
   size_t scales_off, trailer_off, bytes;
+  // fused all-gather (push mode): every payload word is also stored into the
+  // same offset of this rank's slot in each peer's gather buffer (NVLink,
+  // NCCL symmetric window, LSA pointers)
+  int push;
+  ncclWindow_t win;
+  size_t win_off;   // window offset of this rank's slot (same on every rank)
+  int rank, M;
 };
+
+__device__ __forceinline__ void push_u32(const QArgs& a, size_t off, uint32_t v) {
+  for (int q = 0; q < a.M; ++q)
+    if (q != a.rank) *reinterpret_cast<uint32_t*>(ncclGetLsaPointer(a.win, a.win_off + off, q)) = v;
+}
+__device__ __forceinline__ void push_u8(const QArgs& a, size_t off, uint8_t v) {
+  for (int q = 0; q < a.M; ++q)
+    if (q != a.rank) *reinterpret_cast<uint8_t*>(ncclGetLsaPointer(a.win, a.win_off + off, q)) = v;
+}
 
 // Chunk = 1024 elements = 4 rows of 256; lane `lane` owns elements
 // c*1024 + k*256 + 8*lane .. +7 of row k (one LDG.256 per array and row).
@@ -179,7 +203,10 @@ __device__ __forceinline__ void record_first_bad(const QArgs& a, int64_t c, int 
 __device__ __forceinline__ void store_row_codes(const QArgs& a, int64_t c, int k, int lane, uint32_t w,
                                                 bool guard) {
   const int64_t word = (c * 1024 + 256 * k + 8 * lane) >> 3;
-  if (!guard || 4 * (size_t)word < a.scales_off) reinterpret_cast<uint32_t*>(a.slot)[word] = w;
+  if (!guard || 4 * (size_t)word < a.scales_off) {
+    reinterpret_cast<uint32_t*>(a.slot)[word] = w;
+    if (a.push) push_u32(a, 4 * (size_t)word, w);
+  }
 }
 
 // Encodes the 4 rows of a chunk; s[q] = scale of block q of the chunk
@@ -237,10 +264,15 @@ __device__ void write_tail(const QArgs& a) {
   for (size_t o = lo + threadIdx.x; o < a.bytes; o += blockDim.x) {
     if (o >= a.trailer_off && o < a.trailer_off + 16) continue;
     a.slot[o] = 0;
+    if (a.push) push_u8(a, o, 0);
   }
   if (threadIdx.x == 0) {
     *reinterpret_cast<uint32_t*>(a.slot + a.trailer_off) = kMagic;
     *reinterpret_cast<uint32_t*>(a.slot + a.trailer_off + 4) = (uint32_t)a.nb;
+    if (a.push) {
+      push_u32(a, a.trailer_off, kMagic);
+      push_u32(a, a.trailer_off + 4, (uint32_t)a.nb);
+    }
   }
 }
 
@@ -270,7 +302,10 @@ __device__ __forceinline__ void encode_block_rows(const QArgs& a, int64_t c, int
     float sv = s[0];
 #pragma unroll
     for (int q = 1; q < NB; ++q) sv = (lane == q) ? s[q] : sv;
-    if (blk < a.nb) reinterpret_cast<float*>(a.slot + a.scales_off)[blk] = sv;
+    if (blk < a.nb) {
+      reinterpret_cast<float*>(a.slot + a.scales_off)[blk] = sv;
+      if (a.push) push_u32(a, a.scales_off + 4 * (size_t)blk, __float_as_uint(sv));
+    }
   }
 }
 
@@ -369,6 +404,61 @@ __global__ void __launch_bounds__(kThreads) k_encode(QArgs a) {
   for (int64_t c = warp; c < nfull; c += nwarps) encode_chunk<true>(a, c, lane);
   if ((nfull << 10) < a.n && warp == nfull % nwarps) encode_chunk<false>(a, nfull, lane);
   if (blockIdx.x == 0) write_tail(a);
+}
+
+// ---------------------------------------------------------------------------
+// Push-mode all-gather completion (fused into the quantize).
+// k_push_copy: two-pass quantize paths push the finished local slot (scales
+//   written by atomics) to every peer.
+// k_push_signal: after the pushing kernel, publish this rank's first
+//   non-finite index, fence at system scope, then release-store the round id
+//   (the send step t) into flags[rank] of every peer.
+// k_push_wait: block-receive -- acquire-spin until every peer's flag holds t
+//   (bounded: on a timeout the missing peer's slot is marked invalid, the
+//   apply then skips the round and sd_check reports it).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_push_copy(QArgs a) {
+  const size_t n16 = a.bytes / 16;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(a.slot)[i];
+    for (int q = 0; q < a.M; ++q)
+      if (q != a.rank) *reinterpret_cast<uint4*>(ncclGetLsaPointer(a.win, a.win_off + 16 * i, q)) = v;
+  }
+}
+
+__global__ void k_push_signal(QArgs a, size_t flags_off, unsigned long long t) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long fb = *reinterpret_cast<volatile unsigned long long*>(a.slot + a.trailer_off + 8);
+  for (int q = 0; q < a.M; ++q)
+    if (q != a.rank)
+      *reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.win_off + a.trailer_off + 8, q)) = fb;
+  __threadfence_system();
+  for (int q = 0; q < a.M; ++q) {
+    if (q == a.rank) continue;
+    unsigned long long* f =
+        reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, flags_off + 8 * (size_t)a.rank, q));
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(t) : "memory");
+  }
+}
+
+__global__ void k_push_wait(const unsigned long long* flags, uint8_t* half, size_t pb, size_t trailer_off, int M,
+                            int rank, unsigned long long t, unsigned long long timeout_ns,
+                            unsigned long long* status) {
+  const int q = threadIdx.x;
+  if (q >= M || q == rank) return;
+  const unsigned long long t0 = globaltimer_ns();
+  unsigned long long v = 0;
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+    if (v == t) return;
+    if (globaltimer_ns() - t0 > timeout_ns) break;
+    __nanosleep(256);
+  }
+  *reinterpret_cast<volatile uint32_t*>(half + (size_t)q * pb + trailer_off) = 0u;  // invalidate the slot
+  if (status) {
+    volatile unsigned long long* st = status;
+    st[1] = 2ull;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -623,8 +713,8 @@ int grid_for(K kernel, int num_sms, int64_t work_items, int items_per_block) {
 
 }  // namespace
 
-int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, int num_sms,
-                    cudaStream_t st) {
+namespace {
+QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Push& push) {
   QArgs a;
   a.theta = theta;
   a.anchor = anchor;
@@ -635,21 +725,55 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
   a.scales_off = pl.scales_off;
   a.trailer_off = pl.trailer_off;
   a.bytes = pl.bytes;
+  a.push = push.win != nullptr;
+  a.win = push.win;
+  a.win_off = push.win_off;
+  a.rank = push.rank;
+  a.M = push.M;
+  return a;
+}
+
+bool single_pass(int32_t B) { return B == 256 || B == 512 || B == 1024; }
+}  // namespace
+
+int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Push& push,
+                    int num_sms, cudaStream_t st) {
+  const QArgs a = make_qargs(theta, anchor, pl, slot, push);
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int wpb = kThreads / 32;
   int launched = 0;
-  if (pl.B == 256 || pl.B == 512 || pl.B == 1024) {
+  if (single_pass(pl.B)) {
     if (pl.B == 1024) k_quantize<1><<<grid_for(k_quantize<1>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
     else if (pl.B == 512) k_quantize<2><<<grid_for(k_quantize<2>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
     else k_quantize<4><<<grid_for(k_quantize<4>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
     launched = 1;
   } else {
+    QArgs loc = a;
+    loc.push = 0;  // scales come from atomics: build locally, then push the finished slot
     if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
-    k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
-    k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
+    k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
+    k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
     launched = 2;
+    if (a.push) {
+      k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
+      launched = 3;
+    }
   }
   return cudaGetLastError() == cudaSuccess ? launched : -1;
+}
+
+int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_t flags_off, uint64_t t,
+                       cudaStream_t st) {
+  const QArgs a = make_qargs(nullptr, nullptr, pl, slot, push);
+  k_push_signal<<<1, 32, 0, st>>>(a, flags_off, (unsigned long long)t);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
+                     uint64_t timeout_ns, unsigned long long* status, cudaStream_t st) {
+  k_push_wait<<<1, 32, 0, st>>>(flags, half, pl.bytes, pl.trailer_off, M, rank, (unsigned long long)t,
+                                (unsigned long long)timeout_ns, status);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 namespace {
@@ -681,23 +805,14 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 }
 
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
-                          uint8_t* slot, const AdamHyper& hp, int num_sms, cudaStream_t st) {
-  if (!(pl.B == 256 || pl.B == 512 || pl.B == 1024)) {  // two-pass scales: AdamW, then quantize
+                          uint8_t* slot, const AdamHyper& hp, const Push& push, int num_sms, cudaStream_t st) {
+  if (!single_pass(pl.B)) {  // two-pass scales: AdamW, then quantize
     const int k1 = launch_adamw(theta, grad, m, v, pl.n, hp, num_sms, st);
     if (k1 < 0) return -1;
-    const int k2 = launch_quantize(theta, anchor, pl, slot, num_sms, st);
+    const int k2 = launch_quantize(theta, anchor, pl, slot, push, num_sms, st);
     return k2 < 0 ? -1 : k1 + k2;
   }
-  QArgs a;
-  a.theta = theta;
-  a.anchor = anchor;
-  a.n = pl.n;
-  a.nb = pl.nb;
-  a.lgB = ilog2_or_neg(pl.B);
-  a.slot = slot;
-  a.scales_off = pl.scales_off;
-  a.trailer_off = pl.trailer_off;
-  a.bytes = pl.bytes;
+  const QArgs a = make_qargs(theta, anchor, pl, slot, push);
   const AdamArgs h = make_adam(theta, grad, m, v, pl.n, hp);
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int wpb = kThreads / 32;

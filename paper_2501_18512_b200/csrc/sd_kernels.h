@@ -1,6 +1,7 @@
 // sd_kernels.h — launchers of libsd's sm_100a kernels (internal to libsd).
 #pragma once
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <stdint.h>
 
 namespace sdk {
@@ -14,12 +15,31 @@ struct Payload {          // byte offsets inside one replica payload (sd.h)
   size_t bytes;           // total payload bytes
 };
 
+// Push mode (fused all-gather): the quantize also stores every payload word
+// into this rank's slot of each peer's gather buffer through the NCCL
+// symmetric window `win` (window offset win_off).  win == nullptr: local only.
+struct Push {
+  ncclWindow_t win = nullptr;
+  size_t win_off = 0;
+  int rank = 0, M = 1;
+};
+
 // Delta = anchor - theta, per-block absmax, exact E3M0, nibble pack, trailer.
 // slot: one payload (256-aligned).  The trailer's first_bad word must hold
 // 2^64-1 before the launch (sd_outer_grad_quantize memsets it).
 // Returns the number of kernels launched, or -1 on a launch error.
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot,
-                    int num_sms, cudaStream_t st);
+                    const Push& push, int num_sms, cudaStream_t st);
+
+// Push mode completion: publish first_bad to the peers, fence, release-store
+// the round id t into flags[rank] of every peer (window offset flags_off).
+int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_t flags_off, uint64_t t,
+                       cudaStream_t st);
+
+// Push mode block-receive: acquire-wait until every peer's flag == t (at most
+// timeout_ns, then the peer's slot is invalidated and status[1] = 2).
+int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
+                     uint64_t timeout_ns, unsigned long long* status, cudaStream_t st);
 
 // AdamW hyper-parameters with the host-side constants of the op order
 // (bias corrections in binary64 rounded once, DESIGN.md AMB-20).
@@ -38,7 +58,7 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 // AdamW step fused with Delta + E3M0 of the updated theta into one payload
 // (single pass for B in {256, 512, 1024}; AdamW + two-pass quantize otherwise).
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
-                          uint8_t* slot, const AdamHyper& hp, int num_sms, cudaStream_t st);
+                          uint8_t* slot, const AdamHyper& hp, const Push& push, int num_sms, cudaStream_t st);
 
 // Fused decode + M-way fp32 mean + Nesterov + anchor update + alpha-merge.
 // status: host-mapped pinned word pair {first_bad, flags} written when the

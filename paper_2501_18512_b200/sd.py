@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libsd.so")
 SD_ABI_VERSION = 1
 SD_UNIQUE_ID_BYTES = 128
 SD_PAYLOAD_MAGIC = 0x31304453
+SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH, SD_GATHER_AUTO = 0, 1, 2
 
 SD_OK, SD_ERR_ARG, SD_ERR_CONFIG, SD_ERR_SCHEDULE, SD_ERR_STATE, SD_ERR_NONFINITE, SD_ERR_CUDA, SD_ERR_NCCL = range(8)
 STATUS_NAMES = {
@@ -26,7 +27,8 @@ STATUS_NAMES = {
 EXPORTS = (
     "sd_config_default", "sd_config_validate", "sd_fragment_count", "sd_fragment_layout",
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
-    "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free",
+    "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free", "sd_set_gather_mode",
+    "sd_gather_payloads",
     "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync",
     "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
@@ -81,6 +83,8 @@ def lib():
             "sd_init": ([ctypes.POINTER(P), C, I32, I32, P, I32], I32),
             "sd_gather_alloc": ([P, I64, ctypes.POINTER(P)], I32),
             "sd_gather_free": ([P, P], I32),
+            "sd_set_gather_mode": ([P, I32], I32),
+            "sd_gather_payloads": ([P, I32, I64, P, ctypes.POINTER(P)], I32),
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
             "sd_state_prefetch": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
@@ -236,6 +240,15 @@ class SdContext:
         self._c(lib().sd_gather_alloc(self.h, n, ctypes.byref(ptr)))
         nbytes = self.M * sd_payload_bytes(self.cfg, n)
         return _device_bytes(ptr.value, nbytes, self.device if device is None else device)
+
+    def sd_set_gather_mode(self, mode: int):
+        self._c(lib().sd_set_gather_mode(self.h, mode))
+
+    def sd_gather_payloads(self, p, t, buf, n):
+        """-> uint8 view of the M payloads of fragment p's round sent at t"""
+        out = ctypes.c_void_p()
+        self._c(lib().sd_gather_payloads(self.h, p, t, _ptr(buf), ctypes.byref(out)))
+        return _device_bytes(out.value, self.M * sd_payload_bytes(self.cfg, n), self.device)
 
     def sd_gather_free(self, buf):
         self._c(lib().sd_gather_free(self.h, _ptr(buf)))

@@ -14,7 +14,7 @@ from . import sd
 
 class FragmentSync:
     def __init__(self, cfg: sd.SdConfig, frag_numel, rank: int = 0, world: int = 1, device: int = 0,
-                 unique_id: bytes | None = None):
+                 unique_id: bytes | None = None, gather_mode: int = sd.SD_GATHER_AUTO):
         self.cfg = cfg
         self.rank, self.world, self.device = rank, world, device
         self.P = sd.sd_fragment_count(cfg)
@@ -29,6 +29,7 @@ class FragmentSync:
             unique_id = obj[0]
         self.ctx = sd.SdContext(cfg, rank, world, unique_id if world > 1 else None, device)
         self.payload = [sd.sd_payload_bytes(cfg, n) for n in self.n]
+        self.ctx.sd_set_gather_mode(gather_mode)
         # libsd-owned gather buffers: NCCL symmetric memory (copy-engine all-gather, zero SMs)
         # with a communicator; plain device memory otherwise
         self.gather = [self.ctx.sd_gather_alloc(n) for n in self.n]
@@ -36,6 +37,10 @@ class FragmentSync:
     def slot(self, p: int) -> torch.Tensor:
         pb = self.payload[p]
         return self.gather[p][self.rank * pb:(self.rank + 1) * pb]
+
+    def payloads(self, p, t):
+        """uint8 view of the M payloads of fragment p's round sent at t"""
+        return self.ctx.sd_gather_payloads(p, t, self.gather[p], self.n[p])
 
     def outer_state_init(self, p, theta, anchor, momentum, stream=None):
         self.ctx.sd_outer_state_init(theta, anchor, momentum, self.n[p], stream)

@@ -34,7 +34,8 @@ def main():
     P = sd.sd_fragment_count(cfg)
     p = 2
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)
-    fsync = FragmentSync(cfg, [n] * P, rank, world, local)
+    mode = sd.SD_GATHER_PUSH if os.environ.get("SD_TEST_GATHER") == "push" else sd.SD_GATHER_COPY_ENGINE
+    fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode)
     if os.environ.get("SD_TEST_TORCH_BUF") == "1":  # caller-owned (non-symmetric) gather buffers
         fsync.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in fsync.payload]
     A = synth.dev_init(torch.empty(n, device=dev), segs, p)
@@ -57,7 +58,7 @@ def main():
         fsync.receive(p, t + cfg.tau, th, A, v)
         torch.cuda.synchronize()
         got = {}
-        for name, x in (("gather", fsync.gather[p]), ("A", A), ("v", v), ("theta", th)):
+        for name, x in (("gather", fsync.payloads(p, t)), ("A", A), ("v", v), ("theta", th)):
             parts = [torch.empty_like(x) for _ in range(world)]
             dist.all_gather(parts, x)
             got[name] = [q.cpu().numpy() for q in parts]

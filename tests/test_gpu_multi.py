@@ -23,8 +23,8 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False):
-    env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0")
+def _run(nproc, B, torch_buf=False, gather="ce"):
+    env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
@@ -40,8 +40,19 @@ def test_nccl_allgather_two_ranks_bit_exact(B, torch_buf):
     assert rc == 0 and "OK" in out, out[-3000:]
 
 
-def test_nccl_allgather_four_ranks_bit_exact():
+@pytest.mark.parametrize("B", [1024, 0])
+def test_fused_push_gather_two_ranks_bit_exact(B):
+    """SD_GATHER_PUSH: the quantize kernel stores the payload into the peers'
+    buffers over NVLink (fused all-gather); 3 rounds = both buffer halves"""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, B, gather="push")
+    assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push"])
+def test_nccl_allgather_four_ranks_bit_exact(gather):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
-    rc, out = _run(4, 1024)
+    rc, out = _run(4, 1024, gather=gather)
     assert rc == 0 and "OK" in out, out[-3000:]
