@@ -474,3 +474,48 @@ def test_inner_adamw_quantize_fused_bit_exact(n, B):
     assert_same(v_d, v, "v")
     rep.ctx[0].sd_fragment_sync(0, 10, rep.gather, n)
     rep.close()
+
+
+@pytest.mark.parametrize("B", [0, 256, 1024, 4096])
+@pytest.mark.parametrize("n", [1, 9, 1023, 4099, 65536 + 13])
+def test_no_writes_outside_buffers(n, B):
+    """Guard bands (compute-sanitizer is not available on this pool): every
+    array lives between 4 KB canaries; quantize, fused AdamW + quantize and
+    apply must leave the canaries intact (no out-of-bounds writes in the
+    ragged tails)."""
+    G = 1024  # floats of canary on each side
+    M = 2
+    cfg = cfg_for(B)
+    pb = sd.sd_payload_bytes(cfg, n)
+
+    def guarded(x):
+        buf = torch.full((n + 2 * G,), 7.25, device=DEV)
+        buf[G:G + n] = x
+        return buf, buf[G:G + n]
+
+    rng = np.random.default_rng(n + B)
+    A_np = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    Ab = [guarded(to_dev(A_np)) for _ in range(M)]
+    thb = [guarded(to_dev((A_np - 1e-3).astype(np.float32))) for _ in range(M)]
+    vb = [guarded(torch.zeros(n, device=DEV)) for _ in range(M)]
+    gb = [guarded(torch.randn(n, device=DEV) * 1e-3) for _ in range(M)]
+    m1b = [guarded(torch.zeros(n, device=DEV)) for _ in range(M)]
+    m2b = [guarded(torch.zeros(n, device=DEV)) for _ in range(M)]
+    gbuf = torch.full((M * pb + 4096,), 0x5A, dtype=torch.uint8, device=DEV)
+    gather = gbuf[:M * pb]
+    ctx = [sd.SdContext(cfg, m, M, None, 0) for m in range(M)]
+    hp = sd.SdAdamW(**HP)
+    ctx[0].sd_inner_adamw_quantize(0, 10, 1, thb[0][1], gb[0][1], m1b[0][1], m2b[0][1], Ab[0][1], gather[:pb], hp, n)
+    ctx[1].sd_outer_grad_quantize(0, 10, thb[1][1], Ab[1][1], gather[pb:2 * pb], n)
+    for m in range(M):
+        ctx[m].sd_fragment_sync(0, 10, gather, n)
+    for m in range(M):
+        ctx[m].sd_merge(0, 11, gather, thb[m][1], Ab[m][1], vb[m][1], n)
+    torch.cuda.synchronize()
+    for bufs in (Ab, thb, vb, gb, m1b, m2b):
+        for full, _ in bufs:
+            assert torch.all(full[:G] == 7.25) and torch.all(full[G + n:] == 7.25)
+    assert torch.all(gbuf[M * pb:] == 0x5A)
+    for c in ctx:
+        assert c.sd_check()[0] == sd.SD_OK
+        c.sd_finalize()
