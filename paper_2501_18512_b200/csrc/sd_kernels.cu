@@ -130,6 +130,7 @@ struct QArgs {
   int32_t lgB;      // log2(B), or -1 for one block per fragment
   uint8_t* slot;    // payload base
   size_t scales_off, trailer_off, bytes;
+  int64_t c_begin;  // first 1024-element chunk this launch handles (k_quantize tail after the TMA kernel)
   // fused all-gather (push mode): every payload word is also stored into the
   // same offset of this rank's slot in each peer's gather buffer (NVLink,
   // NCCL symmetric window, LSA pointers)
@@ -322,9 +323,113 @@ __global__ void __launch_bounds__(kThreads) k_quantize(QArgs a) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nfull = a.n >> 10;
-  for (int64_t c = warp; c < nfull; c += nwarps) quantize_chunk<NB, true>(a, c, lane);
-  if ((nfull << 10) < a.n && warp == nfull % nwarps) quantize_chunk<NB, false>(a, nfull, lane);
+  for (int64_t c = a.c_begin + warp; c < nfull; c += nwarps) quantize_chunk<NB, true>(a, c, lane);
+  if ((nfull << 10) < a.n && warp == (nfull - a.c_begin) % nwarps) quantize_chunk<NB, false>(a, nfull, lane);
   if (blockIdx.x == 0) write_tail(a);
+}
+
+// ---------------------------------------------------------------------------
+// k_quantize_tma: the same quantize with its input streams staged through
+// shared memory by the bulk-copy engine (cp.async.bulk, 1-D TMA) in a
+// kStages-deep mbarrier pipeline.  One producer warp per CTA issues the bulk
+// copies of a tile (kCW chunks of theta and of A, 2 x 32 KB); kCW consumer
+// warps each take one 1024-element chunk of the stage from shared memory and
+// run the unchanged block-max / encode / store path.  Persistent grid (one
+// CTA per SM); whole tiles only -- the remainder goes to k_quantize.
+// ---------------------------------------------------------------------------
+constexpr int kCW = 8;                       // consumer warps = chunks per tile
+constexpr int kStages = 3;
+constexpr int kTileBytes = kCW * 1024 * 4;   // per array
+constexpr int kTmaThreads = 32 * (kCW + 1);
+constexpr int kTmaSmem = kStages * 2 * kTileBytes + 2 * kStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_quantize_tma(QArgs a, int64_t ntiles) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* sth = reinterpret_cast<float*>(smem);                      // [kStages][kCW*1024]
+  float* san = reinterpret_cast<float*>(smem + kStages * kTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * kTileBytes);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kStages;
+        const uint32_t ph = (uint32_t)(it / kStages) & 1u;
+        mbar_wait(&empty[st], ph ^ 1u);  // slot free (first pass: passes at once)
+        mbar_expect_tx(&full[st], 2 * kTileBytes);
+        const int64_t e0 = tile * (kCW * 1024);
+        bulk_g2s(sth + st * (kCW * 1024), a.theta + e0, kTileBytes, &full[st]);
+        bulk_g2s(san + st * (kCW * 1024), a.anchor + e0, kTileBytes, &full[st]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;  // consumer index = chunk within the tile
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kStages;
+    const uint32_t ph = (uint32_t)(it / kStages) & 1u;
+    mbar_wait(&full[st], ph);
+    const float* th = sth + st * (kCW * 1024) + cw * 1024 + 8 * lane;
+    const float* an = san + st * (kCW * 1024) + cw * 1024 + 8 * lane;
+    f8 d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 t0 = *reinterpret_cast<const float4*>(th + 256 * k);
+      const float4 t1 = *reinterpret_cast<const float4*>(th + 256 * k + 4);
+      const float4 a0 = *reinterpret_cast<const float4*>(an + 256 * k);
+      const float4 a1 = *reinterpret_cast<const float4*>(an + 256 * k + 4);
+      d[k].v[0] = __fsub_rn(a0.x, t0.x);
+      d[k].v[1] = __fsub_rn(a0.y, t0.y);
+      d[k].v[2] = __fsub_rn(a0.z, t0.z);
+      d[k].v[3] = __fsub_rn(a0.w, t0.w);
+      d[k].v[4] = __fsub_rn(a1.x, t1.x);
+      d[k].v[5] = __fsub_rn(a1.y, t1.y);
+      d[k].v[6] = __fsub_rn(a1.z, t1.z);
+      d[k].v[7] = __fsub_rn(a1.w, t1.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // the stage's smem may be refilled
+    encode_block_rows<NB, true>(a, tile * kCW + cw, lane, d);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -725,6 +830,7 @@ QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uin
   a.scales_off = pl.scales_off;
   a.trailer_off = pl.trailer_off;
   a.bytes = pl.bytes;
+  a.c_begin = 0;
   a.push = push.win != nullptr;
   a.win = push.win;
   a.win_off = push.win_off;
@@ -734,6 +840,27 @@ QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uin
 }
 
 bool single_pass(int32_t B) { return B == 256 || B == 512 || B == 1024; }
+
+// SD_QUANTIZE_TMA=1 stages the quantize's input streams through shared memory
+// with bulk copies (k_quantize_tma); default: direct 256-bit loads.
+bool use_tma_quantize() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_QUANTIZE_TMA");
+    v = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int NB>
+void launch_tma(const QArgs& a, int64_t ntiles, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_quantize_tma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    attr = true;
+  }
+  k_quantize_tma<NB><<<grid, kTmaThreads, kTmaSmem, st>>>(a, ntiles);
+}
 }  // namespace
 
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Push& push,
@@ -743,10 +870,21 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
   const int wpb = kThreads / 32;
   int launched = 0;
   if (single_pass(pl.B)) {
-    if (pl.B == 1024) k_quantize<1><<<grid_for(k_quantize<1>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
-    else if (pl.B == 512) k_quantize<2><<<grid_for(k_quantize<2>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
-    else k_quantize<4><<<grid_for(k_quantize<4>, num_sms, chunks, wpb), kThreads, 0, st>>>(a);
-    launched = 1;
+    QArgs t = a;
+    const int64_t ntiles = use_tma_quantize() ? (pl.n >> 10) / kCW : 0;
+    if (ntiles > 0) {  // whole tiles through the bulk-copy pipeline, the rest below
+      const int g = (int)(ntiles < num_sms ? ntiles : num_sms);
+      if (pl.B == 1024) launch_tma<1>(a, ntiles, g, st);
+      else if (pl.B == 512) launch_tma<2>(a, ntiles, g, st);
+      else launch_tma<4>(a, ntiles, g, st);
+      t.c_begin = ntiles * kCW;
+      ++launched;
+    }
+    const int64_t rest = chunks - t.c_begin > 0 ? chunks - t.c_begin : 1;  // >= 1 CTA: write_tail
+    if (pl.B == 1024) k_quantize<1><<<grid_for(k_quantize<1>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
+    else if (pl.B == 512) k_quantize<2><<<grid_for(k_quantize<2>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
+    else k_quantize<4><<<grid_for(k_quantize<4>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
+    ++launched;
   } else {
     QArgs loc = a;
     loc.push = 0;  // scales come from atomics: build locally, then push the finished slot

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsd.so")
+LIB_PATH = os.environ.get("SD_LIBSD") or os.path.join(_HERE, "libsd.so")  # override: experiments only
 
 SD_ABI_VERSION = 1
 SD_UNIQUE_ID_BYTES = 128

@@ -1,0 +1,14 @@
+# A/B of two libsd builds on the same box: default vs $1 (a .so path)
+mkdir -p gpurun_out
+for i in 1 2 3; do
+  for lib in default $1; do
+    if [ "$lib" = default ]; then unset SD_LIBSD; else export SD_LIBSD=$lib; fi
+    python bench.py --steps 256 --no-e2e --no-cpu-baseline --no-m-sweep > gpurun_out/ab.json 2>/dev/null
+    python - $lib <<'PY'
+import json,sys
+j=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1])
+k=j['kernels']
+print(sys.argv[1][-16:], 'value %.4e ms %.4f q %.3f a %.3f'%(j['value'], j['ms_per_step'], k['k_quantize']['frac'], k['k_apply']['frac']))
+PY
+  done
+done
