@@ -616,7 +616,7 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
 def fused_inner_run(torch, sd, sync, cfg, th, A0, n, B, dev, peak, reps=8):
     """NEXT-1: AdamW inner step + quantize as two kernels (28 + 8.5 B/param)
     vs the fused last-inner-step kernel (32.5 B/param: theta stays in
-    registers).  Fragment 0, libsd's k_adamw / k_quantize / k_adamw_quantize."""
+    registers), and AdamW + merge vs the fused receive step.  Fragment 0."""
     import statistics as st
 
     ctx = sync.ctx
@@ -645,12 +645,35 @@ def fused_inner_run(torch, sd, sync, cfg, th, A0, n, B, dev, peak, reps=8):
         if r >= 2:
             sep.append(e[0].elapsed_time(e[1]))
             fus.append(e[2].elapsed_time(e[3]))
+    # the receive step: AdamW + merge (28 + 24.5 B/param) vs fused (44.5: theta once)
+    msep, mfus = [], []
+    for r in range(reps + 2):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ctx.sd_outer_grad_quantize(0, t0, th, A0, slot, n)
+        ctx.sd_fragment_sync(0, t0, sync.gather[0], n)
+        e[0].record()
+        ctx.sd_inner_adamw(r + 1, th, g, m, v, hp, n)
+        ctx.sd_merge(0, t0 + cfg.tau, sync.gather[0], th, A0, mom, n)
+        e[1].record()
+        ctx.sd_outer_grad_quantize(0, t0, th, A0, slot, n)
+        ctx.sd_fragment_sync(0, t0, sync.gather[0], n)
+        e[2].record()
+        ctx.sd_inner_adamw_merge(0, t0 + cfg.tau, r + 1, th, g, m, v, sync.gather[0], A0, mom, hp, n)
+        e[3].record()
+        torch.cuda.synchronize()
+        if r >= 2:
+            msep.append(e[0].elapsed_time(e[1]))
+            mfus.append(e[2].elapsed_time(e[3]))
+    tms, tmf = st.median(msep), st.median(mfus)
     ts, tf = st.median(sep), st.median(fus)
     pay = n / 2 + 4 * (1 if B == 0 else -(-n // B))
     bs, bf = 36 * n + pay, 32 * n + pay
     return {"fragment_elems": int(n), "separate_ms": ts, "fused_ms": tf, "speedup": ts / tf,
             "separate_frac": bs / (ts / 1e3) / 1e9 / peak, "fused_frac": bf / (tf / 1e3) / 1e9 / peak,
-            "algorithmic_bytes_per_elem": {"separate": 36.5, "fused": 32.5}}
+            "algorithmic_bytes_per_elem": {"separate": 36.5, "fused": 32.5},
+            "receive_step": {"separate_ms": tms, "fused_ms": tmf, "speedup": tms / tmf,
+                             "fused_frac": (44 * n + pay) / (tmf / 1e3) / 1e9 / peak,
+                             "algorithmic_bytes_per_elem": {"separate": 52.5, "fused": 44.5}}}
 
 
 def offload_run(torch, sync, A0, v0, n, P, dev, reps=5):

@@ -7,7 +7,8 @@ plain PyTorch (the inner loss L3-4 is not the method); everything from the
 gradients on is libsd: the AdamW inner step (sd_inner_adamw), the fused
 last-inner-step + Delta + E3M0 for the fragment that sends at t
 (sd_inner_adamw_quantize), the copy-engine all-gather (sd_fragment_sync),
-and, tau steps later, decode + fp32 mean + Nesterov + alpha-merge (sd_merge).
+and, tau steps later, the inner step fused with decode + fp32 mean +
+Nesterov + alpha-merge (sd_inner_adamw_merge).
 The model's parameters are views into fragment-contiguous fp32 slabs (AMB-18),
 so libsd operates on the live weights in place.
 
@@ -176,16 +177,21 @@ def main():
         model.collect_grads()
         send, recv = sd.sd_fragment_schedule(cfg, t)
         ev[0].record()
-        for p in range(P):                                                  # L5 (+ L7 fused for senders)
+        fused_recv = [p for p in recv if p not in send]
+        for p in range(P):                                                  # L5, fused with L7 for senders
             if p in send:
                 sync.ctx.sd_inner_adamw_quantize(p, t, t, model.theta[p], model.grad[p], m1[p], m2[p], A[p],
                                                  sync.slot(p), hp, model.n[p])
-            else:
+            elif p not in fused_recv:
                 sync.ctx.sd_inner_adamw(t, model.theta[p], model.grad[p], m1[p], m2[p], hp, model.n[p])
         for p in send:                                                      # L8: async all-gather
             sync.ctx.sd_fragment_sync(p, t, sync.gather[p], model.n[p])
-        for p in recv:                                                      # L10-13
-            sync.receive(p, t, model.theta[p], A[p], vout[p])
+        for p in recv:                                                      # L10-13 (+ L5 fused)
+            if p in fused_recv:
+                sync.ctx.sd_inner_adamw_merge(p, t, t, model.theta[p], model.grad[p], m1[p], m2[p], sync.gather[p],
+                                              A[p], vout[p], hp, model.n[p])
+            else:
+                sync.receive(p, t, model.theta[p], A[p], vout[p])
         ev[1].record()
         if t % args.log_every == 0 or t == args.steps:
             torch.cuda.synchronize()

@@ -257,6 +257,15 @@ sd_status sd_fragment_wait(sd_ctx* ctx, int32_t p, int64_t t, sd_stream stream);
 sd_status sd_merge(sd_ctx* ctx, int32_t p, int64_t t, const void* gather_buf, float* theta,
                    float* anchor, float* momentum, int64_t n, sd_stream stream);
 
+/* The inner step of the receive step fused with its receive (Alg. 2 L5 then
+ * L11-13 at t = send + tau): AdamW on theta (as sd_inner_adamw, step k),
+ * then the same block-receive, mean, Nesterov and alpha-merge as sd_merge
+ * on the updated theta -- theta is read and written once.  On a poisoned
+ * round the AdamW step still happens and the merge is skipped. */
+sd_status sd_inner_adamw_merge(sd_ctx* ctx, int32_t p, int64_t t, int64_t k, float* theta, const float* grad,
+                               float* m, float* v, const void* gather_buf, float* anchor, float* momentum,
+                               int64_t n, const sd_adamw* hp, sd_stream stream);
+
 /* Synchronizes the device and reports deferred errors: CUDA errors, NCCL
  * async errors, and a skipped (poisoned) round — then SD_ERR_NONFINITE and
  * *first_bad_index (if non-NULL) = index of the first non-finite Delta. */

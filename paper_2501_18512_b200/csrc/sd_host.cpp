@@ -744,9 +744,9 @@ sd_status sd_fragment_wait(sd_ctx* c, int32_t p, int64_t t, sd_stream stream) {
   return issue_push_wait(c, p, static_cast<cudaStream_t>(stream));
 }
 
-sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
-                   float* momentum, int64_t n, sd_stream stream) {
-  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+namespace {
+sd_status do_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
+                   float* momentum, int64_t n, cudaStream_t s, const sdk::AdamInner* inner) {
   sd_status st;
   if ((st = check_fragment(c, p, t, n))) return st;
   const int64_t s_step = receive_send_step(&c->cfg, p, t);
@@ -764,17 +764,39 @@ sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
                 (st = check_ptr(c, momentum, 32, "momentum"))))
     return st;
   const sdk::Payload pl = payload_of(&c->cfg, n);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
   if ((st = issue_push_wait(c, p, s))) return st;
   const uint8_t* payloads = static_cast<const uint8_t*>(gather_buf) + (f.push ? f.half_off : 0);
-  const int k = sdk::launch_apply(payloads, pl, c->M, theta, anchor, momentum,
-                                  c->cfg.outer_lr, c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s);
+  const int k = sdk::launch_apply(payloads, pl, c->M, theta, anchor, momentum, c->cfg.outer_lr,
+                                  c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s, inner);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_apply launch");
   g_launches += (uint64_t)k;
   f = Inflight();
   return SD_OK;
+}
+}  // namespace
+
+sd_status sd_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, float* theta, float* anchor,
+                   float* momentum, int64_t n, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  return do_merge(c, p, t, gather_buf, theta, anchor, momentum, n, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+sd_status sd_inner_adamw_merge(sd_ctx* c, int32_t p, int64_t t, int64_t k, float* theta, const float* grad,
+                               float* m, float* v, const void* gather_buf, float* anchor, float* momentum,
+                               int64_t n, const sd_adamw* hp, sd_stream stream) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  sdk::AdamInner in;
+  sd_status st = adam_hyper(c, k, hp, &in.hp);
+  if (st != SD_OK) return st;
+  if (n > 0 && ((st = check_ptr(c, grad, 32, "grad")) || (st = check_ptr(c, m, 32, "m")) ||
+                (st = check_ptr(c, v, 32, "v"))))
+    return st;
+  in.grad = grad;
+  in.m = m;
+  in.v = v;
+  return do_merge(c, p, t, gather_buf, theta, anchor, momentum, n, static_cast<cudaStream_t>(stream), &in);
 }
 
 sd_status sd_check(sd_ctx* c, int64_t* first_bad_index) {

@@ -719,8 +719,8 @@ __device__ __forceinline__ void outer_step(float S, float& a, float& w, float& t
   t = __fadd_rn(__fmul_rn(p.alpha, t), __fmul_rn(p.beta, a));                      // alpha merge
 }
 
-template <int kM>
-__global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
+template <int kM, bool kAdam>
+__global__ void __launch_bounds__(kThreads) k_apply(AArgs p, AdamArgs h) {
   __shared__ int skip;
   const int M = kM > 0 ? kM : p.M;
   if (threadIdx.x == 0) {
@@ -740,14 +740,26 @@ __global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
     }
   }
   __syncthreads();
-  if (skip) return;
+  if (skip && !kAdam) return;  // poisoned round: nothing changes (with kAdam the inner step still runs)
 
   const int64_t n8 = p.n >> 3;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += nthr) {
+    f8 t = kAdam ? ld8(p.theta + 8 * i) : ld8_stream(p.theta + 8 * i);
+    if (kAdam) {  // the inner step of this step first (Alg. 2 L5 precedes L10-13)
+      const f8 g = ld8_stream(h.grad + 8 * i);
+      f8 m1 = ld8(h.m + 8 * i), m2 = ld8(h.v + 8 * i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) adamw_one(t.v[j], g.v[j], m1.v[j], m2.v[j], h);
+      st8(h.m + 8 * i, m1);
+      st8(h.v + 8 * i, m2);
+      if (skip) {
+        st8(p.theta + 8 * i, t);
+        continue;
+      }
+    }
     f8 a = ld8(p.A + 8 * i);
     f8 w = ld8(p.v + 8 * i);
-    f8 t = ld8_stream(p.theta + 8 * i);
     const int64_t blk = p.lgB < 0 ? 0 : ((8 * i) >> p.lgB);
     float S[8];
 #pragma unroll 8
@@ -769,6 +781,17 @@ __global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
   // ragged tail: the last n % 8 elements, one thread each
   if (blockIdx.x == 0 && threadIdx.x < (p.n & 7)) {
     const int64_t e = (n8 << 3) + threadIdx.x;
+    float t = p.theta[e];
+    if (kAdam) {
+      float m1 = h.m[e], m2 = h.v[e];
+      adamw_one(t, h.grad[e], m1, m2, h);
+      h.m[e] = m1;
+      h.v[e] = m2;
+      if (skip) {
+        p.theta[e] = t;
+        return;
+      }
+    }
     const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
     float S = 0.0f;
     for (int m = 0; m < M; ++m) {
@@ -778,7 +801,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(AArgs p) {
       decode8(c, reinterpret_cast<const float*>(slot + p.scales_off)[blk], q);
       S = (m == 0) ? q[0] : __fadd_rn(S, q[0]);
     }
-    float a = p.A[e], w = p.v[e], t = p.theta[e];
+    float a = p.A[e], w = p.v[e];
     outer_step(S, a, w, t, p);
     p.A[e] = a;
     p.v[e] = w;
@@ -964,7 +987,8 @@ int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, c
 }
 
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor, float* momentum,
-                 float lr, float mu, float alpha, unsigned long long* status, int num_sms, cudaStream_t st) {
+                 float lr, float mu, float alpha, unsigned long long* status, int num_sms, cudaStream_t st,
+                 const AdamInner* inner) {
   AArgs p;
   p.gather = gather;
   p.pb = pl.bytes;
@@ -983,14 +1007,22 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.pow2M = (M & (M - 1)) == 0;
   p.invM = 1.0f / (float)M;  // exact when M is a power of two
   p.status = status;
+  AdamArgs h{};
+  if (inner) h = make_adam(theta, inner->grad, inner->m, inner->v, pl.n, inner->hp);
   const int64_t items = (pl.n >> 3) > 0 ? (pl.n >> 3) : 1;
+#define SD_APPLY_CASE(KM)                                                                                         \
+  if (inner)                                                                                                      \
+    k_apply<KM, true><<<grid_for(k_apply<KM, true>, num_sms, items, kThreads), kThreads, 0, st>>>(p, h);          \
+  else                                                                                                            \
+    k_apply<KM, false><<<grid_for(k_apply<KM, false>, num_sms, items, kThreads), kThreads, 0, st>>>(p, h);
   switch (M) {
-    case 1: k_apply<1><<<grid_for(k_apply<1>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
-    case 2: k_apply<2><<<grid_for(k_apply<2>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
-    case 4: k_apply<4><<<grid_for(k_apply<4>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
-    case 8: k_apply<8><<<grid_for(k_apply<8>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
-    default: k_apply<0><<<grid_for(k_apply<0>, num_sms, items, kThreads), kThreads, 0, st>>>(p); break;
+    case 1: SD_APPLY_CASE(1) break;
+    case 2: SD_APPLY_CASE(2) break;
+    case 4: SD_APPLY_CASE(4) break;
+    case 8: SD_APPLY_CASE(8) break;
+    default: SD_APPLY_CASE(0) break;
   }
+#undef SD_APPLY_CASE
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

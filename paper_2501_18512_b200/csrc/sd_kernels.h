@@ -63,8 +63,16 @@ int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, c
 // Fused decode + M-way fp32 mean + Nesterov + anchor update + alpha-merge.
 // status: host-mapped pinned word pair {first_bad, flags} written when the
 // round is skipped.  Returns kernels launched or -1.
+// inner: optional AdamW step applied to theta first (the step's inner update
+// fused with the receive; theta is read and written once).
+struct AdamInner {
+  const float* grad;
+  float* m;
+  float* v;
+  AdamHyper hp;
+};
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor,
                  float* momentum, float lr, float mu, float alpha, unsigned long long* status,
-                 int num_sms, cudaStream_t st);
+                 int num_sms, cudaStream_t st, const AdamInner* inner = nullptr);
 
 }  // namespace sdk

@@ -30,7 +30,7 @@ EXPORTS = (
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free", "sd_set_gather_mode",
     "sd_gather_payloads",
     "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync",
-    "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
+    "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_inner_adamw_merge", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
 
@@ -95,6 +95,7 @@ def lib():
             "sd_fragment_sync": ([P, I32, I64, P, I64, P], I32),
             "sd_fragment_wait": ([P, I32, I64, P], I32),
             "sd_merge": ([P, I32, I64, P, P, P, P, I64, P], I32),
+            "sd_inner_adamw_merge": ([P, I32, I64, I64, P, P, P, P, P, P, P, I64, ctypes.POINTER(SdAdamW), P], I32),
             "sd_check": ([P, pI64], I32),
             "sd_last_error": ([P], ctypes.c_char_p),
             "sd_finalize": ([P], I32),
@@ -293,6 +294,13 @@ class SdContext:
     def sd_merge(self, p, t, gather_buf, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n
         self._c(lib().sd_merge(self.h, p, t, _ptr(gather_buf), _ptr(theta), _ptr(anchor), _ptr(momentum), n, _stream(stream)))
+
+    def sd_inner_adamw_merge(self, p, t, k, theta, grad, m, v, gather_buf, anchor, momentum, hp: SdAdamW, n=None,
+                             stream=None):
+        n = theta.numel() if n is None else n
+        self._c(lib().sd_inner_adamw_merge(self.h, p, t, k, _ptr(theta), _ptr(grad), _ptr(m), _ptr(v),
+                                           _ptr(gather_buf), _ptr(anchor), _ptr(momentum), n, ctypes.byref(hp),
+                                           _stream(stream)))
 
     def sd_check(self):
         """-> (status, first_bad_index); does not raise on SD_ERR_NONFINITE"""

@@ -519,3 +519,41 @@ def test_no_writes_outside_buffers(n, B):
     for c in ctx:
         assert c.sd_check()[0] == sd.SD_OK
         c.sd_finalize()
+
+
+@pytest.mark.parametrize("M", [1, 2, 3])
+@pytest.mark.parametrize("poison", [False, True])
+def test_inner_adamw_merge_fused_bit_exact(M, poison):
+    """The receive step's inner AdamW fused with the merge equals
+    or_adamw followed by or_apply (merge skipped, AdamW kept, if poisoned)."""
+    n, B = 8 * 1024 + 3, 1024
+    rng = np.random.default_rng(M * 10 + poison)
+    cfg = cfg_for(B)
+    rep = EmulatedReplicas(cfg, M, n)
+    A0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    sends = [(A0 - rng.standard_normal(n).astype(np.float32) * 1e-3).astype(np.float32) for _ in range(M)]
+    if poison:
+        sends[M - 1][123] = np.inf
+    th_live = (A0 - np.float32(5e-4)).astype(np.float32)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    m1 = (rng.standard_normal(n) * 1e-4).astype(np.float32)
+    m2 = (rng.random(n) * 1e-7).astype(np.float32)
+    v0 = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    A_d = [to_dev(A0) for _ in range(M)]
+    rep.quantize_all(0, 10, [to_dev(x) for x in sends], A_d)
+    th_d, m1_d, m2_d, v_d = to_dev(th_live), to_dev(m1), to_dev(m2), to_dev(v0)
+    hp = sd.SdAdamW(**HP)
+    rep.ctx[0].sd_inner_adamw_merge(0, 11, 5, th_d, to_dev(g), m1_d, m2_d, rep.gather, A_d[0], v_d, hp, n)
+    for m in range(1, M):
+        rep.ctx[m].sd_merge(0, 11, rep.gather, to_dev(th_live), A_d[m], to_dev(v0), n)
+    torch.cuda.synchronize()
+    th_o, A_o, v_o = th_live.copy(), A0.copy(), v0.copy()
+    oracle.adamw(th_o, g, m1, m2, 5, lr=HP["lr"], b1=HP["beta1"], b2=HP["beta2"], eps=HP["eps"], wd=HP["weight_decay"])
+    st = oracle.apply(rep.gather.cpu().numpy(), M, n, B, A_o, v_o, th_o)
+    assert st == (1 if poison else 0)
+    assert_same(th_d, th_o, "theta")
+    assert_same(m1_d, m1, "adam m")
+    assert_same(m2_d, m2, "adam v")
+    assert_same(A_d[0], A_o, "anchor")
+    assert_same(v_d, v_o, "momentum")
+    rep.close()
