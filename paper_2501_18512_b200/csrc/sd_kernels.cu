@@ -318,7 +318,9 @@ __device__ __forceinline__ void quantize_chunk(const QArgs& a, int64_t c, int la
 }
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads) k_quantize(QArgs a) {
+// 3 resident CTAs per SM (<= 85 registers, no spills): 24 warps with 8 KB of
+// loads in flight each; measured 211 vs 222 us per 1B fragment at 2 CTAs/SM.
+__global__ void __launch_bounds__(kThreads, 3) k_quantize(QArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -501,7 +503,7 @@ __device__ __forceinline__ void encode_chunk(const QArgs& a, int64_t c, int lane
   encode_chunk_rows<1, kFullChunk>(a, c, lane, d, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_encode(QArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_encode(QArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -720,7 +722,10 @@ __device__ __forceinline__ void outer_step(float S, float& a, float& w, float& t
 }
 
 template <int kM, bool kAdam>
-__global__ void __launch_bounds__(kThreads) k_apply(AArgs p, AdamArgs h) {
+#ifndef SD_APPLY_MINB
+#define SD_APPLY_MINB 4  // <= 64 registers, no spills: M = 8 apply 1.03 vs 0.975 at 3 CTAs/SM (B200 A/B)
+#endif
+__global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, AdamArgs h) {
   __shared__ int skip;
   const int M = kM > 0 ? kM : p.M;
   if (threadIdx.x == 0) {
