@@ -166,18 +166,20 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  *                         word into this rank's slot of each peer's buffer
  *                         over NVLink as it produces it (NCCL symmetric-window
  *                         LSA pointers), then release-signals a per-round
- *                         flag; the block-receive is an acquire-wait on the
- *                         peers' flags.  Buffers hold two rounds (alternating
- *                         by send index), so no rendezvous is needed.
+ *                         flag with the round id (the count of sends of
+ *                         this fragment, the same on every rank); the
+ *                         block-receive is an acquire-wait on the peers'
+ *                         flags.  Buffers hold two rounds (alternating by
+ *                         round id), so no rendezvous is needed.
  * With caller-owned buffers or without a communicator the mode is ignored. */
 #define SD_GATHER_COPY_ENGINE 0
 #define SD_GATHER_PUSH 1
 #define SD_GATHER_AUTO 2 /* default: PUSH when tau == 0 (nothing to overlap the gather with), else COPY_ENGINE */
 sd_status sd_set_gather_mode(sd_ctx* ctx, int32_t mode);
 
-/* Address of the M payloads of fragment p's round sent at step t inside
- * gather_buf (the buffer itself, or its round-parity half in push mode). */
-sd_status sd_gather_payloads(sd_ctx* ctx, int32_t p, int64_t t, const void* gather_buf, const void** out);
+/* Address of the M payloads of fragment p's most recent round inside
+ * gather_buf (the buffer itself, or that round's half in push mode). */
+sd_status sd_gather_payloads(sd_ctx* ctx, int32_t p, const void* gather_buf, const void** out);
 
 /* Outer-state store init (§8(a) a2; AMB-2): anchor <- theta, momentum <- 0. */
 sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, float* momentum,

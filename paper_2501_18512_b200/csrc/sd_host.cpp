@@ -125,6 +125,7 @@ struct Inflight {
   bool push = false;      // payloads were pushed by the quantize (fused all-gather)
   bool waited = false;    // push mode: the block-receive wait kernel was issued
   size_t half_off = 0;    // push mode: byte offset of this round's half
+  uint64_t seq = 0;       // push mode: round id published in the peers' flags
 };
 
 }  // namespace
@@ -143,6 +144,7 @@ struct sd_ctx {
   sd_config cfg;
   std::vector<GatherBuf> bufs;
   int32_t gather_mode = SD_GATHER_AUTO;
+  std::vector<uint64_t> round_seq;  // push mode: sends of each fragment so far (round id, same on every rank)
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -320,6 +322,7 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   c->device = device;
   c->P = num_fragments(cfg);
   c->fl.resize((size_t)c->P);
+  c->round_seq.assign((size_t)c->P, 0);
   auto bail = [&](sd_status s) {
     sd_finalize(c);
     return s;
@@ -410,16 +413,13 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   return SD_OK;
 }
 
-sd_status sd_gather_payloads(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, const void** out) {
+sd_status sd_gather_payloads(sd_ctx* c, int32_t p, const void* gather_buf, const void** out) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
   if (!out) return ctx_fail(c, SD_ERR_ARG, "out pointer is NULL");
   if (p < 0 || p >= c->P) return ctx_fail(c, SD_ERR_ARG, "fragment %d out of range [0, %d)", p, c->P);
   *out = gather_buf;
   GatherBuf* b = find_buf(c, gather_buf);
-  if (b && b->push) {
-    const int64_t round = (t - offset_of(&c->cfg, p)) / c->cfg.H;
-    *out = static_cast<const char*>(b->ptr) + (size_t)(round & 1) * b->half;
-  }
+  if (b && b->push) *out = static_cast<const char*>(b->ptr) + (size_t)(c->round_seq[p] & 1) * b->half;
   return SD_OK;
 }
 
@@ -531,6 +531,7 @@ namespace {
 struct PushRound {
   GatherBuf* buf = nullptr;
   size_t half_off = 0;
+  uint64_t seq = 0;
   sdk::Push push;
 };
 
@@ -540,9 +541,10 @@ sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk:
   if (b->pb != pl.bytes) return ctx_fail(c, SD_ERR_ARG, "gather buffer was allocated for payloads of %zu bytes, not %zu", b->pb, pl.bytes);
   if (static_cast<char*>(slot_out) != static_cast<char*>(b->ptr) + (size_t)c->rank * pl.bytes)
     return ctx_fail(c, SD_ERR_ARG, "slot_out must be gather_buf + rank * payload");
-  const int64_t round = (t - offset_of(&c->cfg, p)) / c->cfg.H;  // send index of fragment p
+  (void)t;
+  r->seq = c->round_seq[p] + 1;  // this send's round id (identical on every rank: same call sequence)
   r->buf = b;
-  r->half_off = (size_t)(round & 1) * b->half;
+  r->half_off = (size_t)(r->seq & 1) * b->half;
   r->push.win = b->win;
   r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
   r->push.rank = c->rank;
@@ -584,9 +586,10 @@ sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, c
                    const sdk::Payload& pl, cudaStream_t s) {
   if (pr.buf) {  // fused all-gather: publish this round to the peers
     const int k = sdk::launch_push_signal(pl, local_slot(c, slot_out, pr, pl), pr.push,
-                                          pr.half_off + (size_t)c->M * pl.bytes, (uint64_t)t, s);
+                                          pr.half_off + (size_t)c->M * pl.bytes, pr.seq, s);
     if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_signal launch");
     g_launches += (uint64_t)k;
+    c->round_seq[p] = pr.seq;
   }
   c->fl[p].state = QUANTIZED;
   c->fl[p].send_step = t;
@@ -595,6 +598,7 @@ sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, c
   c->fl[p].push = pr.buf != nullptr;
   c->fl[p].waited = false;
   c->fl[p].half_off = pr.half_off;
+  c->fl[p].seq = pr.seq;
   return SD_OK;
 }
 
@@ -719,7 +723,7 @@ sd_status issue_push_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
   const sdk::Payload pl = payload_of(&c->cfg, f.n);
   uint8_t* half = static_cast<uint8_t*>(b->ptr) + f.half_off;
   const int k = sdk::launch_push_wait(reinterpret_cast<const unsigned long long*>(half + (size_t)c->M * pl.bytes),
-                                      half, pl, c->M, c->rank, (uint64_t)f.send_step, 30ull * 1000000000ull,
+                                      half, pl, c->M, c->rank, f.seq, 30ull * 1000000000ull,
                                       c->status_dev, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_wait launch");
   g_launches += (uint64_t)k;

@@ -519,8 +519,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_encode(QArgs a) {
 //   written by atomics) to every peer.
 // k_push_signal: after the pushing kernel, publish this rank's first
 //   non-finite index, fence at system scope, then release-store the round id
-//   (the send step t) into flags[rank] of every peer.
-// k_push_wait: block-receive -- acquire-spin until every peer's flag holds t
+//   (count of sends of the fragment, same on every rank) into flags[rank] of
+//   every peer.
+// k_push_wait: block-receive -- acquire-spin until every peer's flag holds it
 //   (bounded: on a timeout the missing peer's slot is marked invalid, the
 //   apply then skips the round and sd_check reports it).
 // ---------------------------------------------------------------------------

@@ -32,11 +32,11 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
                     const Push& push, int num_sms, cudaStream_t st);
 
 // Push mode completion: publish first_bad to the peers, fence, release-store
-// the round id t into flags[rank] of every peer (window offset flags_off).
+// the round id into flags[rank] of every peer (window offset flags_off).
 int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_t flags_off, uint64_t t,
                        cudaStream_t st);
 
-// Push mode block-receive: acquire-wait until every peer's flag == t (at most
+// Push mode block-receive: acquire-wait until every peer's flag == the round id t (at most
 // timeout_ns, then the peer's slot is invalidated and status[1] = 2).
 int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
                      uint64_t timeout_ns, unsigned long long* status, cudaStream_t st);

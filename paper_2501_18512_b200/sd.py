@@ -84,7 +84,7 @@ def lib():
             "sd_gather_alloc": ([P, I64, ctypes.POINTER(P)], I32),
             "sd_gather_free": ([P, P], I32),
             "sd_set_gather_mode": ([P, I32], I32),
-            "sd_gather_payloads": ([P, I32, I64, P, ctypes.POINTER(P)], I32),
+            "sd_gather_payloads": ([P, I32, P, ctypes.POINTER(P)], I32),
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
             "sd_state_prefetch": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
@@ -245,10 +245,10 @@ class SdContext:
     def sd_set_gather_mode(self, mode: int):
         self._c(lib().sd_set_gather_mode(self.h, mode))
 
-    def sd_gather_payloads(self, p, t, buf, n):
-        """-> uint8 view of the M payloads of fragment p's round sent at t"""
+    def sd_gather_payloads(self, p, buf, n):
+        """-> uint8 view of the M payloads of fragment p's most recent round"""
         out = ctypes.c_void_p()
-        self._c(lib().sd_gather_payloads(self.h, p, t, _ptr(buf), ctypes.byref(out)))
+        self._c(lib().sd_gather_payloads(self.h, p, _ptr(buf), ctypes.byref(out)))
         return _device_bytes(out.value, self.M * sd_payload_bytes(self.cfg, n), self.device)
 
     def sd_gather_free(self, buf):

@@ -38,9 +38,9 @@ class FragmentSync:
         pb = self.payload[p]
         return self.gather[p][self.rank * pb:(self.rank + 1) * pb]
 
-    def payloads(self, p, t):
-        """uint8 view of the M payloads of fragment p's round sent at t"""
-        return self.ctx.sd_gather_payloads(p, t, self.gather[p], self.n[p])
+    def payloads(self, p):
+        """uint8 view of the M payloads of fragment p's most recent round"""
+        return self.ctx.sd_gather_payloads(p, self.gather[p], self.n[p])
 
     def outer_state_init(self, p, theta, anchor, momentum, stream=None):
         self.ctx.sd_outer_state_init(theta, anchor, momentum, self.n[p], stream)

@@ -48,8 +48,8 @@ def main():
         A_o = synth.host_init(segs, p)
         v_o = np.zeros(n, np.float32)
         th_o = [A_o.copy() for _ in range(world)]
-    for r in range(1, 4):
-        t = r * cfg.H + t_p
+    for r in range(1, 6):
+        t = min(r, 3) * cfg.H + t_p  # rounds 4, 5 repeat step t of round 3 (round ids must not rely on t)
         assert p in sd.sd_fragment_schedule(cfg, t)[0]
         synth.dev_apply_window(th, segs, p, rank, r)
         fsync.send(p, t, th, A)
@@ -58,7 +58,7 @@ def main():
         fsync.receive(p, t + cfg.tau, th, A, v)
         torch.cuda.synchronize()
         got = {}
-        for name, x in (("gather", fsync.payloads(p, t)), ("A", A), ("v", v), ("theta", th)):
+        for name, x in (("gather", fsync.payloads(p)), ("A", A), ("v", v), ("theta", th)):
             parts = [torch.empty_like(x) for _ in range(world)]
             dist.all_gather(parts, x)
             got[name] = [q.cpu().numpy() for q in parts]
