@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="1B", choices=["toy", "35M", "1B", "4B"])
     ap.add_argument("--scale-block", type=int, default=1024)
+    ap.add_argument("--tau", type=int, default=None, help="override the workload's tau (configs[4] sweep)")
+    ap.add_argument("--fragment-size", type=int, default=None, help="override |p| in layers (configs[4] sweep)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -139,6 +141,17 @@ def calendar_sends(sd, cfg, count: int):
     return out[:count]
 
 
+def workload_with_overrides(wl, args):
+    import dataclasses
+
+    kw = {}
+    if args.tau is not None:
+        kw["tau"] = args.tau
+    if args.fragment_size is not None:
+        kw["fragment_size"] = args.fragment_size
+    return dataclasses.replace(wl, **kw) if kw else wl
+
+
 def make_cfg(sd, wl, B):
     return sd.sd_config_default(wl.layers, wl.fragment_size, wl.H, tau=wl.tau, alpha=wl.alpha, outer_lr=wl.lr,
                                 outer_momentum=wl.mu, scale_block=B)
@@ -193,7 +206,7 @@ def run_reference(args):
     from synth.workloads import WORKLOADS
     from paper_2501_18512_b200 import sd
 
-    wl = WORKLOADS[args.workload]
+    wl = workload_with_overrides(WORKLOADS[args.workload], args)
     B = args.scale_block
     cfg = make_cfg(sd, wl, B)
     P = sd.sd_fragment_count(cfg)
@@ -246,7 +259,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    wl = WORKLOADS[args.workload]
+    wl = workload_with_overrides(WORKLOADS[args.workload], args)
     B = args.scale_block
     M = world
     cfg = make_cfg(sd, wl, B)
@@ -320,7 +333,7 @@ def main():
             sync.ctx.sd_fragment_wait(pp, tt + cfg.tau)
             sync.ctx.sd_merge(pp, tt + cfg.tau, sync.gather[pp], theta[pp], A[pp], v[pp], n[pp])
 
-    pipelined = P > 1 and not args.serial
+    pipelined = P > 1 and not args.serial and cfg.tau > 0  # tau = 0: the receive is in the send's step
     step_fn = pipe_step if pipelined else one_step
 
     # L2 policy: the 1B/4B state (12 B/param, GBs) streams through HBM; small
@@ -458,11 +471,11 @@ def main():
 
     # ---- gather hidden behind tau synthetic inner steps? (N > 1 only)
     overlap = None
-    if world > 1:
+    if world > 1 and cfg.tau > 0:
         overlap = {}
         for i, kind in enumerate(("adamw", "gemm")):
-            base = 5 * (W + K) + 24 * i
-            evs = calendar_sends(sd, cfg, base + 24)[base:]
+            base = 5 * (W + K) + 32 * i
+            evs = calendar_sends(sd, cfg, base + 32)[base:]
             overlap[kind] = overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, evs, dev,
                                         kind=kind)
 
@@ -532,7 +545,7 @@ def main():
     return 0
 
 
-def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=4,
+def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=7,
                 kind="adamw"):
     """SURVEY.md §8(d) hidden-gather check on the real NCCL path: per round,
     quantize -> all-gather on the comm stream while the compute stream runs
@@ -603,7 +616,8 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
         over.append(maxr(e[4].elapsed_time(e[5])))
         bytes_in.append((world - 1) * sync.payload[p])
     ta, tg, to = st.median(alone), st.median(gath), st.median(over)
-    exposed = max(0.0, to - ta)
+    # paired estimate: each rep measures the inner steps alone and with the gather back to back
+    exposed = max(0.0, st.median([o - a for o, a in zip(over, alone)]))
     gbps = st.median(bytes_in) / (tg / 1e3) / 1e9
     return {"tau": tau, "inner_step": ("AdamW-shaped synthetic pass over the whole replica, 24 B/param (synth/)"
                                        if kind == "adamw" else "4 bf16 8192^3 cuBLAS matmuls (SM-bound)"),
