@@ -557,3 +557,39 @@ def test_inner_adamw_merge_fused_bit_exact(M, poison):
     assert_same(A_d[0], A_o, "anchor")
     assert_same(v_d, v_o, "momentum")
     rep.close()
+
+
+def test_cuda_graph_capture_replay_matches_eager():
+    """A step captured as a CUDA graph (libsd's calls are capturable) and
+    replayed gives the same bits as issuing it eagerly again."""
+    n, M = 20000 + 3, 1
+    rng = np.random.default_rng(77)
+    A0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    th0 = (A0 - rng.standard_normal(n).astype(np.float32) * 1e-3).astype(np.float32)
+    cfg = cfg_for(1024)
+    outs = []
+    for mode in ("eager", "graph"):
+        ctx = sd.SdContext(cfg, 0, M, None, 0)
+        gather = torch.empty(sd.sd_payload_bytes(cfg, n), dtype=torch.uint8, device=DEV)
+        A, v, th = to_dev(A0), torch.zeros(n, device=DEV), to_dev(th0)
+
+        def step():
+            ctx.sd_outer_grad_quantize(0, 10, th, A, gather, n)
+            ctx.sd_fragment_sync(0, 10, gather, n)
+            ctx.sd_merge(0, 11, gather, th, A, v, n)
+
+        if mode == "eager":
+            for _ in range(3):
+                step()
+        else:
+            step()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()  # captured (second round) ...
+            g.replay()  # ... and executed, then once more
+            g.replay()
+        torch.cuda.synchronize()
+        outs.append([bits(x) for x in (A, v, th)])
+        ctx.sd_finalize()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
