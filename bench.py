@@ -199,9 +199,10 @@ def cpu_baseline(wl, B, M, order, segs, n, target_s):
     total_t, total_e, used = 0.0, 0, []
     for p in order:
         S = int(min(n[p], budget - total_e))
-        S -= S % 1024 if S > 1024 else 0
-        if S <= 0:
+        S -= S % 1024
+        if S < (1 << 20) and total_e > 0:  # not worth another fragment's input generation
             break
+        S = max(S, min(n[p], 1024))
         dt, _ = oracle_sample_rate(wl, B, M, p, segs[p], S)
         total_t += dt
         total_e += S
