@@ -144,6 +144,7 @@ def main():
     ap.add_argument("--tau", type=int, default=1)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--log-every", type=int, default=20)
+    ap.add_argument("--amp", action="store_true", help="bf16 autocast for the forward/backward (weights stay fp32)")
     args = ap.parse_args()
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -172,7 +173,8 @@ def main():
     outer_ms, t0 = 0.0, time.time()
     for t in range(1, args.steps + 1):
         x, y = synthetic_batch(gen, args.batch, args.seq, args.vocab, perm)
-        total, loss = model.forward(x, y)                                   # Alg. 2 L3-4
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=args.amp):
+            total, loss = model.forward(x, y)                               # Alg. 2 L3-4
         total.backward()
         model.collect_grads()
         send, recv = sd.sd_fragment_schedule(cfg, t)
