@@ -375,6 +375,18 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   return SD_OK;
 }
 
+namespace {
+void release(sd_ctx* c, GatherBuf& b) {
+  if (b.nccl) {
+    if (b.win) ncclCommWindowDeregister(c->comm, b.win);
+    ncclMemFree(b.ptr);
+  } else if (b.ptr) {
+    cudaFree(b.ptr);
+  }
+  b = GatherBuf();
+}
+}  // namespace
+
 sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
   if (!out) return ctx_fail(c, SD_ERR_ARG, "out pointer is NULL");
@@ -404,9 +416,20 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   } else {
     SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
   }
-  if (b.push) {  // round flags start at 0 (never a send step)
+  if (b.push) {  // round flags start at 0 (never a round id)
     SD_CUDA(c, cudaMemset(b.ptr, 0, b.bytes));
     SD_CUDA(c, cudaDeviceSynchronize());
+  } else if (c->comm) {
+    // one full-size all-gather now: NCCL sets up the symmetric-window
+    // copy-engine collective lazily (~0.4 s on the first call), which would
+    // otherwise stall the host inside the first sd_fragment_sync
+    ncclResult_t r = ncclAllGather(static_cast<char*>(b.ptr) + (size_t)c->rank * b.pb, b.ptr, b.pb, ncclUint8,
+                                   c->comm, c->comm_stream);
+    if (r != ncclSuccess) {
+      release(c, b);
+      return ctx_fail(c, SD_ERR_NCCL, "warm-up ncclAllGather: %s", ncclGetErrorString(r));
+    }
+    SD_CUDA(c, cudaStreamSynchronize(c->comm_stream));
   }
   c->bufs.push_back(b);
   *out = b.ptr;
@@ -434,17 +457,7 @@ sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
   return SD_OK;
 }
 
-namespace {
-void release(sd_ctx* c, GatherBuf& b) {
-  if (b.nccl) {
-    if (b.win) ncclCommWindowDeregister(c->comm, b.win);
-    ncclMemFree(b.ptr);
-  } else if (b.ptr) {
-    cudaFree(b.ptr);
-  }
-  b = GatherBuf();
-}
-}  // namespace
+
 
 sd_status sd_gather_free(sd_ctx* c, void* gather_buf) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
