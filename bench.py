@@ -62,9 +62,9 @@ def parse():
     ap.add_argument("--serial", action="store_true", help="no send/receive pipelining across fragments")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as a CUDA graph (auto: single GPU, L2-resident small configs)")
-    ap.add_argument("--gather", choices=["auto", "ce", "push"], default="auto",
-                    help="all-gather: NCCL copy engines (ce), fused into the quantize kernel (push), "
-                         "or libsd's choice (auto: push iff tau == 0)")
+    ap.add_argument("--gather", choices=["auto", "ce", "push", "pull"], default="auto",
+                    help="all-gather: NCCL copy engines (ce), fused into the quantize kernel (push) or into "
+                         "the merge kernel (pull), or libsd's choice (auto)")
     return ap.parse_args()
 
 
@@ -295,7 +295,7 @@ def main():
         theta.append(th)
     sync = FragmentSync(cfg, n, rank, world, local,
                         gather_mode={"auto": sd.SD_GATHER_AUTO, "ce": sd.SD_GATHER_COPY_ENGINE,
-                                     "push": sd.SD_GATHER_PUSH}[args.gather])
+                                     "push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}[args.gather])
     torch.cuda.synchronize()
 
     K, W = args.steps, max(1, args.warmup)
@@ -559,7 +559,10 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
             "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n],
-                           gather=("fused into k_quantize: NVLink stores to the peers' symmetric buffers + "
+                           gather=("fused into k_apply: NVLink loads of the peers' payloads + flag handshake"
+                                   if (args.gather == "pull" or (args.gather == "auto" and cfg.tau == 0 and
+                                                                 world in (4, 8))) else
+                                   "fused into k_quantize: NVLink stores to the peers' symmetric buffers + "
                                    "flag handshake" if (args.gather == "push" or
                                                         (args.gather == "auto" and cfg.tau == 0)) else
                                    "NCCL in-place all-gather on copy engines (symmetric window, zero CTAs)"),

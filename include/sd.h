@@ -174,7 +174,11 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  * With caller-owned buffers or without a communicator the mode is ignored. */
 #define SD_GATHER_COPY_ENGINE 0
 #define SD_GATHER_PUSH 1
-#define SD_GATHER_AUTO 2 /* default: PUSH when tau == 0 (nothing to overlap the gather with), else COPY_ENGINE */
+#define SD_GATHER_AUTO 2 /* default: COPY_ENGINE when tau >= 1 (hidden behind later work); with tau == 0
+                            (nothing to overlap with) PULL for M in {4, 8}, else PUSH -- measured on B200 */
+#define SD_GATHER_PULL 3 /* fused into the apply: the quantize writes locally and signals; the merge
+                            kernel reads the peers' payloads from their buffers over NVLink (no HBM
+                            staging of the M payloads); M in {2, 4, 8}, else COPY_ENGINE */
 sd_status sd_set_gather_mode(sd_ctx* ctx, int32_t mode);
 
 /* Address of the M payloads of fragment p's most recent round inside

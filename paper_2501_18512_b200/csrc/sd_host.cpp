@@ -122,7 +122,8 @@ struct Inflight {
   int64_t n = 0;
   const void* slot = nullptr;
   const void* gather = nullptr;
-  bool push = false;      // payloads were pushed by the quantize (fused all-gather)
+  bool push = false;      // two-round symmetric buffer with round flags (PUSH or PULL mode)
+  bool pull = false;      // PULL: the apply reads the peers' slots over NVLink
   bool waited = false;    // push mode: the block-receive wait kernel was issued
   size_t half_off = 0;    // push mode: byte offset of this round's half
   uint64_t seq = 0;       // push mode: round id published in the peers' flags
@@ -135,7 +136,8 @@ struct GatherBuf {
   size_t bytes = 0;
   ncclWindow_t win = nullptr;
   bool nccl = false;
-  bool push = false;   // fused-push layout: two halves (round parity) of M payloads + M round flags
+  bool push = false;   // two-round layout: halves (round parity) of M payloads + M round flags (PUSH/PULL)
+  bool pull = false;   // PULL mode: peers' payloads stay in the peers' buffers, read by the apply
   size_t half = 0;     // bytes per half
   size_t pb = 0;       // payload bytes
 };
@@ -397,7 +399,15 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   b.pb = payload_of(&c->cfg, n).bytes;
   // measured on B200: the fused push wins when the gather is on the
   // critical path (tau = 0); with tau >= 1 the copy-engine gather is hidden
-  b.push = c->comm && (c->gather_mode == SD_GATHER_PUSH || (c->gather_mode == SD_GATHER_AUTO && c->cfg.tau == 0));
+  // AUTO, from B200 measurements: with tau >= 1 the copy-engine
+  // gather hides behind the next kernels; with tau = 0 it is on the critical
+  // path and a fused variant wins -- the push at M = 2, the pull at M = 4, 8
+  int mode = c->gather_mode;
+  if (mode == SD_GATHER_AUTO)
+    mode = c->cfg.tau > 0 ? SD_GATHER_COPY_ENGINE : ((c->M == 4 || c->M == 8) ? SD_GATHER_PULL : SD_GATHER_PUSH);
+  if (mode == SD_GATHER_PULL && !(c->M == 2 || c->M == 4 || c->M == 8)) mode = SD_GATHER_COPY_ENGINE;
+  b.push = c->comm && (mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL);
+  b.pull = b.push && mode == SD_GATHER_PULL;
   if (b.push) {
     b.half = (size_t)align_up((int64_t)(b.pb * (size_t)c->M) + 256, 256);
     b.bytes = (size_t)align_up((int64_t)(2 * b.half), 2 << 20);
@@ -448,9 +458,8 @@ sd_status sd_gather_payloads(sd_ctx* c, int32_t p, const void* gather_buf, const
 
 sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
-  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO)
-    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH or SD_GATHER_AUTO",
-                    mode);
+  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO && mode != SD_GATHER_PULL)
+    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, _PUSH, _PULL or _AUTO", mode);
   for (const Inflight& f : c->fl)
     if (f.state != IDLE) return ctx_fail(c, SD_ERR_STATE, "gather mode changed while a fragment is in flight");
   c->gather_mode = mode;
@@ -545,6 +554,7 @@ struct PushRound {
   GatherBuf* buf = nullptr;
   size_t half_off = 0;
   uint64_t seq = 0;
+  bool pull = false;
   sdk::Push push;
 };
 
@@ -558,10 +568,13 @@ sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk:
   r->seq = c->round_seq[p] + 1;  // this send's round id (identical on every rank: same call sequence)
   r->buf = b;
   r->half_off = (size_t)(r->seq & 1) * b->half;
-  r->push.win = b->win;
-  r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
-  r->push.rank = c->rank;
-  r->push.M = c->M;
+  if (!b->pull) {  // PUSH: the quantize stores into the peers' buffers
+    r->push.win = b->win;
+    r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
+    r->push.rank = c->rank;
+    r->push.M = c->M;
+  }
+  r->pull = b->pull;
   return SD_OK;
 }
 
@@ -598,7 +611,12 @@ sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const 
 sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, const PushRound& pr,
                    const sdk::Payload& pl, cudaStream_t s) {
   if (pr.buf) {  // fused all-gather: publish this round to the peers
-    const int k = sdk::launch_push_signal(pl, local_slot(c, slot_out, pr, pl), pr.push,
+    sdk::Push sig = pr.push;  // the signal reaches every peer in both modes
+    sig.win = pr.buf->win;
+    sig.win_off = pr.half_off + (size_t)c->rank * pl.bytes;
+    sig.rank = c->rank;
+    sig.M = c->M;
+    const int k = sdk::launch_push_signal(pl, local_slot(c, slot_out, pr, pl), sig,
                                           pr.half_off + (size_t)c->M * pl.bytes, pr.seq, s);
     if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_signal launch");
     g_launches += (uint64_t)k;
@@ -609,6 +627,7 @@ sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, c
   c->fl[p].n = n;
   c->fl[p].slot = slot_out;
   c->fl[p].push = pr.buf != nullptr;
+  c->fl[p].pull = pr.pull;
   c->fl[p].waited = false;
   c->fl[p].half_off = pr.half_off;
   c->fl[p].seq = pr.seq;
@@ -785,8 +804,16 @@ sd_status do_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
   if ((st = issue_push_wait(c, p, s))) return st;
   const uint8_t* payloads = static_cast<const uint8_t*>(gather_buf) + (f.push ? f.half_off : 0);
+  sdk::Pull pull;
+  if (f.pull) {
+    GatherBuf* b = find_buf(c, gather_buf);
+    pull.win = b ? b->win : nullptr;
+    pull.half_off = f.half_off;
+    pull.rank = c->rank;
+  }
   const int k = sdk::launch_apply(payloads, pl, c->M, theta, anchor, momentum, c->cfg.outer_lr,
-                                  c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s, inner);
+                                  c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s, inner,
+                                  f.pull ? &pull : nullptr);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_apply launch");
   g_launches += (uint64_t)k;
   f = Inflight();

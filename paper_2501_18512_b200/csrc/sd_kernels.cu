@@ -687,7 +687,24 @@ struct AArgs {
   float lr, mu, alpha, beta, invM;
   int pow2M;
   unsigned long long* status;
+  // pull mode: slot m lives in rank m's own buffer (symmetric window); the
+  // LSA mapping makes slot m = base0 + m * (peer stride + payload)
+  int pull;
+  ncclWindow_t win;
+  size_t half_off;
 };
+
+__device__ __forceinline__ void slot_geometry(const AArgs& p, const uint8_t*& base, size_t& stride) {
+  if (p.pull) {
+    const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 0));
+    const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 1));
+    base = b0;
+    stride = (size_t)(b1 - b0) + p.pb;
+  } else {
+    base = p.gather;
+    stride = p.pb;
+  }
+}
 
 // Decodes 8 codes (nibble i = element i) into LUT values +-2^(e-7) (codes 0
 // and 8 -> +0) times s.  The LUT value's top 16 bits are the
@@ -729,11 +746,14 @@ template <int kM, bool kAdam>
 __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, AdamArgs h) {
   __shared__ int skip;
   const int M = kM > 0 ? kM : p.M;
+  const uint8_t* gbase;
+  size_t gstride;
+  slot_geometry(p, gbase, gstride);
   if (threadIdx.x == 0) {
     unsigned long long fb = ~0ull;
     int badmagic = 0;
     for (int m = 0; m < M; ++m) {
-      const uint8_t* tr = p.gather + (size_t)m * p.pb + p.trailer_off;
+      const uint8_t* tr = gbase + (size_t)m * gstride + p.trailer_off;
       if (*reinterpret_cast<const uint32_t*>(tr) != kMagic) badmagic = 1;
       const unsigned long long f = *reinterpret_cast<const unsigned long long*>(tr + 8);
       fb = f < fb ? f : fb;
@@ -770,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, Adam
     float S[8];
 #pragma unroll 8
     for (int m = 0; m < M; ++m) {
-      const uint8_t* slot = p.gather + (size_t)m * p.pb;
+      const uint8_t* slot = gbase + (size_t)m * gstride;
       const uint32_t code = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
       const float s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
       float q[8];
@@ -801,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, Adam
     const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
     float S = 0.0f;
     for (int m = 0; m < M; ++m) {
-      const uint8_t* slot = p.gather + (size_t)m * p.pb;
+      const uint8_t* slot = gbase + (size_t)m * gstride;
       const uint32_t c = (slot[e >> 1] >> ((e & 1) * 4)) & 15u;
       float q[8];
       decode8(c, reinterpret_cast<const float*>(slot + p.scales_off)[blk], q);
@@ -994,7 +1014,7 @@ int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, c
 
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor, float* momentum,
                  float lr, float mu, float alpha, unsigned long long* status, int num_sms, cudaStream_t st,
-                 const AdamInner* inner) {
+                 const AdamInner* inner, const Pull* pull) {
   AArgs p;
   p.gather = gather;
   p.pb = pl.bytes;
@@ -1013,6 +1033,9 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.pow2M = (M & (M - 1)) == 0;
   p.invM = 1.0f / (float)M;  // exact when M is a power of two
   p.status = status;
+  p.pull = pull != nullptr && pull->win != nullptr;
+  p.win = p.pull ? pull->win : nullptr;
+  p.half_off = p.pull ? pull->half_off : 0;
   AdamArgs h{};
   if (inner) h = make_adam(theta, inner->grad, inner->m, inner->v, pl.n, inner->hp);
   const int64_t items = (pl.n >> 3) > 0 ? (pl.n >> 3) : 1;

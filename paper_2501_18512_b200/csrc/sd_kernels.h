@@ -71,8 +71,15 @@ struct AdamInner {
   float* v;
   AdamHyper hp;
 };
+// Pull mode: slot m != rank is read from rank m's own buffer over NVLink
+// (symmetric window, LSA pointers) at window offset half_off + m * payload.
+struct Pull {
+  ncclWindow_t win = nullptr;
+  size_t half_off = 0;
+  int rank = 0;
+};
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor,
                  float* momentum, float lr, float mu, float alpha, unsigned long long* status,
-                 int num_sms, cudaStream_t st, const AdamInner* inner = nullptr);
+                 int num_sms, cudaStream_t st, const AdamInner* inner = nullptr, const Pull* pull = nullptr);
 
 }  // namespace sdk

@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
 N=${1:-2}
 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/pytest_push_$N.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_push_$N.log
-for g in ce push; do
+for g in ${GATHERS:-ce push pull}; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2956$N bench.py --gpus $N --gather $g --no-e2e > gpurun_out/bench_n${N}_$g.json 2> gpurun_out/bench_n${N}_$g.err; echo "bench $g rc=$?"
   python - gpurun_out/bench_n${N}_$g.json <<'PY'
 import json,sys

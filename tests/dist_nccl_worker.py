@@ -34,7 +34,8 @@ def main():
     P = sd.sd_fragment_count(cfg)
     p = 2
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)
-    mode = sd.SD_GATHER_PUSH if os.environ.get("SD_TEST_GATHER") == "push" else sd.SD_GATHER_COPY_ENGINE
+    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}.get(os.environ.get("SD_TEST_GATHER"),
+                                                                    sd.SD_GATHER_COPY_ENGINE)
     fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode)
     if os.environ.get("SD_TEST_TORCH_BUF") == "1":  # caller-owned (non-symmetric) gather buffers
         fsync.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in fsync.payload]
@@ -58,7 +59,9 @@ def main():
         fsync.receive(p, t + cfg.tau, th, A, v)
         torch.cuda.synchronize()
         got = {}
-        for name, x in (("gather", fsync.payloads(p)), ("A", A), ("v", v), ("theta", th)):
+        pb = fsync.payload[p]
+        own = fsync.payloads(p)[rank * pb:(rank + 1) * pb]  # each rank's own slot (valid in every mode)
+        for name, x in (("gather", own), ("A", A), ("v", v), ("theta", th)):
             parts = [torch.empty_like(x) for _ in range(world)]
             dist.all_gather(parts, x)
             got[name] = [q.cpu().numpy() for q in parts]
@@ -70,8 +73,8 @@ def main():
                 synth.host_apply_drift(th_o[m], segs, p, m, r)
             st, g_o = oracle.round_(sends, th_o, A_o, v_o, B=B)
             assert st == 0
+            ok &= np.array_equal(np.concatenate(got["gather"]), g_o)
             for m in range(world):
-                ok &= np.array_equal(got["gather"][m], g_o)
                 ok &= np.array_equal(got["A"][m].view(np.uint32), A_o.view(np.uint32))
                 ok &= np.array_equal(got["v"][m].view(np.uint32), v_o.view(np.uint32))
                 ok &= np.array_equal(got["theta"][m].view(np.uint32), th_o[m].view(np.uint32))

@@ -50,7 +50,17 @@ def test_fused_push_gather_two_ranks_bit_exact(B):
     assert rc == 0 and "OK" in out, out[-3000:]
 
 
-@pytest.mark.parametrize("gather", ["ce", "push"])
+@pytest.mark.parametrize("B", [1024, 0])
+def test_fused_pull_gather_two_ranks_bit_exact(B):
+    """SD_GATHER_PULL: the merge kernel reads the peers' payloads from their
+    own buffers over NVLink (no HBM staging), after the round-flag handshake"""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, B, gather="pull")
+    assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
 def test_nccl_allgather_four_ranks_bit_exact(gather):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
