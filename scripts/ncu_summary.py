@@ -35,6 +35,32 @@ if os.path.exists(lst):
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         unit = 1e-3 if max(v) > 1e4 else 1.0  # ns vs us
         lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) * unit:.1f} | {sum(v) / tot:.3f} |")
+def emu_traffic(rep, traffic):
+    """k_apply<M, ...> rows of the emulated-M capture -> traffic keys for M = 2, 4, 8."""
+    import re
+
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    if len(rows) < 3:
+        return []
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    ik, ir, iw, it = (hdr.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                              "gpu__time_duration.sum"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out = []
+    for r in data:
+        m = re.search(r"k_apply<(\d+)", r[ik])
+        if not m:
+            continue
+        M = int(m.group(1))
+        rd = float(r[ir].replace(",", "")) * scale.get(units[ir], 1)
+        wr = float(r[iw].replace(",", "")) * scale.get(units[iw], 1)
+        traffic[f"k_apply/{workload.split('/')[0]}/M{M}/B1024"] = {"dram_bytes_per_launch": rd + wr, "read": rd,
+                                                                 "write": wr, "source": rep.split("/")[-1]}
+        out.append((M, float(r[it].replace(",", "")), rd, wr))
+    return out
+
+
 rep = os.path.join(g, f"prof_{tag}.ncu-rep")
 traffic = {}
 tpath = os.path.join(out, "ncu_traffic.json")
@@ -63,6 +89,19 @@ if os.path.exists(rep):
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * scale.get(units[idx["dram__bytes_write.sum"]], 1)
         traffic[f"{name}/{workload}"] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
                                          "source": rep.split("/")[-1]}
+    emu = os.path.join(g, f"prof_emu_{tag}.ncu-rep")
+    if os.path.exists(emu):
+        rows = emu_traffic(emu, traffic)
+        if rows:
+            lines.append(f"\n## k_apply with M emulated payloads ({emu.split('/')[-1]}, 1B fragment, n = 151,007,616)\n")
+            lines.append("| M | duration (us) | dram read (GB) | dram write (GB) | algorithmic (GB) |\n|---|---|---|---|---|")
+            seen = set()
+            for M, dur, rd, wr in rows:
+                if M in seen:
+                    continue
+                seen.add(M)
+                alg = (24 + M * 0.50390625) * 151007616 / 1e9
+                lines.append(f"| {M} | {dur:.1f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | {alg:.3f} |")
     json.dump(traffic, open(tpath, "w"), indent=1)
 open(os.path.join(out, f"ncu_{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
