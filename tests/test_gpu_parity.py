@@ -213,18 +213,24 @@ def test_schedule_and_state_errors():
 
 
 # ---------------------------------------------------------------- toy, e2e
-def test_toy_config_alg2_end_to_end():
-    """BASELINE.json configs[0]: M=2, 2^20 fp32 params in 2 fragments, H=10,
-    tau=1, T=100.  Every step: synthetic inner step on each replica, then the
-    calendar's sends and receives through libsd; final theta (both
-    replicas), anchors and momenta bit-identical to or_toy_run."""
-    M, bl, H, tau, T = 2, 2 ** 19, 10, 1, 100
-    c_or = oracle.config(L=2, fs=1, H=H, tau=tau, T=T)
+@pytest.mark.parametrize("L,fs,H,tau,T,M,bl", [
+    (2, 1, 10, 1, 100, 2, 2 ** 19),      # BASELINE.json configs[0]
+    (1, 1, 5, 0, 23, 3, 3000),           # DiLoCo (Alg. 1): P = 1, tau = 0, M = 3
+    (6, 2, 12, 0, 50, 2, 4096 + 4),      # tau = 0 with 3 strided fragments, ragged (n = 8200)
+    (4, 1, 9, 8, 40, 4, 2048),           # tau = H - 1, flush at T
+])
+def test_toy_config_alg2_end_to_end(L, fs, H, tau, T, M, bl):
+    """Alg. 2 end to end.  configs[0]: M=2, 2^20 fp32 params in 2 fragments,
+    H=10, tau=1, T=100; plus the degenerate schedules.  Every step: synthetic
+    inner step on each replica, then the calendar's sends and receives
+    through libsd; final theta (every replica), anchors and momenta
+    bit-identical to or_toy_run."""
+    c_or = oracle.config(L=L, fs=fs, H=H, tau=tau, T=T)
     th_o, A_o, v_o, sent_o, st = oracle.toy_run(c_or, M, bl, synth.SEED)
     assert st == 0
-    cfg = sd.sd_config_default(2, 1, H, tau=tau, T=T)
+    cfg = sd.sd_config_default(L, fs, H, tau=tau, T=T)
     P = sd.sd_fragment_count(cfg)
-    n = bl
+    n = fs * bl
     reps = [EmulatedReplicas(cfg, M, n) for _ in range(P)]
     A = [[synth.dev_init(torch.empty(n, device=DEV), synth.flat_segments(n), p) for _ in range(M)] for p in range(P)]
     v = [[torch.zeros(n, device=DEV) for _ in range(M)] for p in range(P)]
