@@ -771,6 +771,19 @@ __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, Adam
   const int64_t n8 = p.n >> 3;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += nthr) {
+    // payload words first: in pull mode M-1 of them come over NVLink (longest latency)
+    constexpr int kMr = kM > 0 ? kM : 1;
+    uint32_t code[kMr];
+    float scl[kMr];
+    const int64_t blk = p.lgB < 0 ? 0 : ((8 * i) >> p.lgB);
+    if (kM > 0 && !(kAdam && skip)) {
+#pragma unroll
+      for (int m = 0; m < kMr; ++m) {
+        const uint8_t* slot = gbase + (size_t)m * gstride;
+        code[m] = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
+        scl[m] = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
+      }
+    }
     f8 t = kAdam ? ld8(p.theta + 8 * i) : ld8_stream(p.theta + 8 * i);
     if (kAdam) {  // the inner step of this step first (Alg. 2 L5 precedes L10-13)
       const f8 g = ld8_stream(h.grad + 8 * i);
@@ -786,15 +799,21 @@ __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, Adam
     }
     f8 a = ld8(p.A + 8 * i);
     f8 w = ld8(p.v + 8 * i);
-    const int64_t blk = p.lgB < 0 ? 0 : ((8 * i) >> p.lgB);
     float S[8];
 #pragma unroll 8
     for (int m = 0; m < M; ++m) {
-      const uint8_t* slot = gbase + (size_t)m * gstride;
-      const uint32_t code = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
-      const float s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
+      uint32_t cw;
+      float s;
+      if (kM > 0) {
+        cw = code[m];
+        s = scl[m];
+      } else {
+        const uint8_t* slot = gbase + (size_t)m * gstride;
+        cw = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
+        s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
+      }
       float q[8];
-      decode8(code, s, q);
+      decode8(cw, s, q);
 #pragma unroll
       for (int j = 0; j < 8; ++j) S[j] = (m == 0) ? q[j] : __fadd_rn(S[j], q[j]);  // ascending m
     }
