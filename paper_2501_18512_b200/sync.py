@@ -32,7 +32,17 @@ class FragmentSync:
         self.ctx.sd_set_gather_mode(gather_mode)
         # libsd-owned gather buffers: NCCL symmetric memory (copy-engine all-gather, zero SMs)
         # with a communicator; plain device memory otherwise
-        self.gather = [self.ctx.sd_gather_alloc(n) for n in self.n]
+        self.gather = []
+        for n, pb in zip(self.n, self.payload):
+            try:
+                self.gather.append(self.ctx.sd_gather_alloc(n))
+            except sd.SdError as e:  # no symmetric memory here: caller-owned buffer, NCCL SM-kernel gather
+                import sys
+
+                import torch
+
+                print(f"[FragmentSync] sd_gather_alloc failed ({e}); using a plain device buffer", file=sys.stderr)
+                self.gather.append(torch.empty(world * pb, dtype=torch.uint8, device=torch.device("cuda", device)))
 
     def slot(self, p: int) -> torch.Tensor:
         pb = self.payload[p]
