@@ -66,3 +66,15 @@ def test_nccl_allgather_four_ranks_bit_exact(gather):
         pytest.skip("needs 4 GPUs")
     rc, out = _run(4, 1024, gather=gather)
     assert rc == 0 and "OK" in out, out[-3000:]
+
+
+def test_fsdp_composition_two_replicas_two_shards():
+    """M = 2 replicas x G = 2 shards on 4 GPUs, one libsd
+    communicator per shard group; equals the unsharded oracle round."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_fsdp_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "OK" in out, out[-3000:]
