@@ -171,7 +171,9 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  *                         block-receive is an acquire-wait on the peers'
  *                         flags.  Buffers hold two rounds (alternating by
  *                         round id), so no rendezvous is needed.
- * With caller-owned buffers or without a communicator the mode is ignored. */
+ * With caller-owned buffers or without a communicator the mode is ignored.
+ * In PUSH and PULL modes a gather buffer must serve a single fragment (its
+ * round ids count that fragment's sends). */
 #define SD_GATHER_COPY_ENGINE 0
 #define SD_GATHER_PUSH 1
 #define SD_GATHER_AUTO 2 /* default: COPY_ENGINE when tau >= 1 (hidden behind later work); with tau == 0

@@ -397,8 +397,6 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   SD_CUDA(c, cudaSetDevice(c->device));
   GatherBuf b;
   b.pb = payload_of(&c->cfg, n).bytes;
-  // measured on B200: the fused push wins when the gather is on the
-  // critical path (tau = 0); with tau >= 1 the copy-engine gather is hidden
   // AUTO, from B200 measurements: with tau >= 1 the copy-engine
   // gather hides behind the next kernels; with tau = 0 it is on the critical
   // path and a fused variant wins -- the push at M = 2, the pull at M = 4, 8
@@ -465,8 +463,6 @@ sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
   c->gather_mode = mode;
   return SD_OK;
 }
-
-
 
 sd_status sd_gather_free(sd_ctx* c, void* gather_buf) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
