@@ -599,3 +599,47 @@ def test_cuda_graph_capture_replay_matches_eager():
         ctx.sd_finalize()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def test_many_rounds_wide_dynamic_range():
+    """40 rounds, M = 3, every scale block scaled by 2^k with k uniform in
+    [-140, 100] (subnormal to huge scales, both encode paths, underflowing
+    decodes): payloads and outer state stay bit-identical to the oracle."""
+    rng = np.random.default_rng(2025)
+    n, M, B = 16 * 1024 + 9, 3, 1024
+    cfg = cfg_for(B, alpha=0.25, lr=0.4, mu=0.9)
+    rep = EmulatedReplicas(cfg, M, n)
+    A_o = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    v_o = np.zeros(n, np.float32)
+    A_d = [to_dev(A_o) for _ in range(M)]
+    v_d = [torch.zeros(n, device=DEV) for _ in range(M)]
+    nb = -(-n // B)
+    for r in range(40):
+        sends, merges = [], []
+        for m in range(M):
+            d = edge_deltas(n, B, rng).astype(np.float64)
+            for b in range(nb):
+                d[b * B:(b + 1) * B] *= 2.0 ** int(rng.integers(-140, 101))
+            d = np.clip(d, -3e38, 3e38).astype(np.float32)
+            th = (A_o - d).astype(np.float32)
+            th = np.where(np.isfinite(th), th, A_o).astype(np.float32)
+            sends.append(th)
+            merges.append((th * np.float32(0.5)).astype(np.float32))
+        t = 10 * (r + 1)
+        rep.quantize_all(0, t, [to_dev(x) for x in sends], A_d)
+        th_d = [to_dev(x) for x in merges]
+        rep.merge_all(0, t + 1, th_d, A_d, v_d)
+        mo = [x.copy() for x in merges]
+        st, g_o = oracle.round_(sends, mo, A_o, v_o, B=B, lr=0.4, mu=0.9, alpha=0.25)
+        torch.cuda.synchronize()
+        if st != 0:  # a non-finite Delta (huge scale overflow) poisons the round on both sides
+            assert all(s[0] == sd.SD_ERR_NONFINITE for s in rep.check_all())
+            A_o = A_d[0].cpu().numpy()
+            v_o = v_d[0].cpu().numpy()
+            continue
+        assert np.array_equal(rep.gather.cpu().numpy(), g_o), f"round {r}: payload bytes differ"
+        for m in range(M):
+            assert_same(A_d[m], A_o, f"round {r} anchor")
+            assert_same(v_d[m], v_o, f"round {r} momentum")
+            assert_same(th_d[m], mo[m], f"round {r} theta")
+    rep.close()
