@@ -415,6 +415,17 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   if (c->comm) {
     ncclResult_t r = ncclMemAlloc(&b.ptr, b.bytes);
     if (r != ncclSuccess) return ctx_fail(c, SD_ERR_NCCL, "ncclMemAlloc(%zu): %s", b.bytes, ncclGetErrorString(r));
+    if (b.push) {
+      // round flags start at 0 (never a round id).  Zeroed BEFORE the
+      // collective registration: once any rank returns from it, every rank
+      // has finished its memset, so no peer's first push can be overwritten
+      cudaError_t e = cudaMemset(b.ptr, 0, b.bytes);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        ncclMemFree(b.ptr);
+        return cuda_fail(c, e, "cudaMemset(gather flags)");
+      }
+    }
     r = ncclCommWindowRegister(c->comm, b.ptr, b.bytes, &b.win, NCCL_WIN_COLL_SYMMETRIC);
     if (r != ncclSuccess) {
       ncclMemFree(b.ptr);
@@ -424,10 +435,7 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   } else {
     SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
   }
-  if (b.push) {  // round flags start at 0 (never a round id)
-    SD_CUDA(c, cudaMemset(b.ptr, 0, b.bytes));
-    SD_CUDA(c, cudaDeviceSynchronize());
-  } else if (c->comm) {
+  if (!b.push && c->comm) {
     // one full-size all-gather now: NCCL sets up the symmetric-window
     // copy-engine collective lazily (~0.4 s on the first call), which would
     // otherwise stall the host inside the first sd_fragment_sync
@@ -437,7 +445,11 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
       release(c, b);
       return ctx_fail(c, SD_ERR_NCCL, "warm-up ncclAllGather: %s", ncclGetErrorString(r));
     }
-    SD_CUDA(c, cudaStreamSynchronize(c->comm_stream));
+    const cudaError_t e = cudaStreamSynchronize(c->comm_stream);
+    if (e != cudaSuccess) {
+      release(c, b);
+      return cuda_fail(c, e, "warm-up ncclAllGather");
+    }
   }
   c->bufs.push_back(b);
   *out = b.ptr;
