@@ -123,6 +123,54 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(win), "window": window}
 
 
+# --------------------------------------------------------------------------- host link
+def pcie_probe(host, dev_buf, s_in, s_out, reps=5):
+    """The host link's ceiling for e2e: pinned H2D alone, D2H alone, and both
+    at once on two streams (full duplex), best of `reps`, GB/s per direction."""
+    import torch
+    nbytes = 4 * host.numel()
+    res = {}
+    for kind in ("h2d", "d2h", "duplex"):
+        best = 0.0
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            if kind in ("h2d", "duplex"):
+                s_in.wait_event(a)
+                with torch.cuda.stream(s_in):
+                    dev_buf.copy_(host, non_blocking=True)
+            if kind in ("d2h", "duplex"):
+                tmp = host if kind == "d2h" else _probe_pinned(host)
+                s_out.wait_event(a)
+                with torch.cuda.stream(s_out):
+                    tmp.copy_(dev_buf if kind == "d2h" else _probe_dev(dev_buf), non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s_in)
+            torch.cuda.current_stream().wait_stream(s_out)
+            b.record()
+            torch.cuda.synchronize()
+            best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+        res[kind + "_gbs"] = best
+    return res
+
+
+_PROBE = {}
+
+
+def _probe_pinned(like):
+    import torch
+    if "h" not in _PROBE:
+        _PROBE["h"] = torch.empty_like(like, pin_memory=True)
+    return _PROBE["h"]
+
+
+def _probe_dev(like):
+    import torch
+    if "d" not in _PROBE:
+        _PROBE["d"] = torch.empty_like(like)
+    return _PROBE["d"]
+
+
 # --------------------------------------------------------------------------- workload
 def algorithmic_bytes(n: int, M: int, B: int):
     """quantize reads theta, A (8 B) and writes 0.5 B of codes
@@ -535,7 +583,9 @@ def main():
         e2e = {"value": eel * world / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * eel // K, "d2h_bytes_per_step": 4 * eel // K,
                "ms_per_step": ems / K, "path": ("pinned host theta -> H2D -> sd_* C-ABI calls -> D2H for every step's fragment; "
-                        "copies of neighbouring fragments overlap (two copy streams)")}
+                        "copies of neighbouring fragments overlap (two copy streams)"),
+               "link_gbs_each_way": 4 * eel / (ems / 1e3) / 1e9,
+               "pcie_probe": pcie_probe(host[0], theta[0], h2d_s, d2h_s)}
     sampler.stop()
     clocks = sampler.summary(w0, w1)
     clocks["remeasured_after_throttle"] = remeasured
