@@ -316,6 +316,67 @@ def test_full_size_sampled_blocks(shape):
     rep.close()
 
 
+@pytest.mark.parametrize("B", [1024, 4096])
+def test_fragment_beyond_2_31_elements(B):
+    """Maximum sizes: one fragment of 2.42e9 elements (3 layers at d = 8192;
+    every fp32 array > 8 GiB, byte offsets > 2^33), M = 2 emulated, the
+    one-pass (B = 1024) and two-pass (B = 4096) quantize.  Sampled
+    scale blocks -- including those at element 2^30, 2^31 and the ragged
+    tail -- are bit-identical to the oracle: no 32-bit index or offset
+    anywhere in the quantize, the slot stride or the apply."""
+    segs = synth.fragment_segments(8192, [0, 1, 2], False)
+    segs = np.concatenate([segs, np.array([(int(synth.segments_numel(segs)), 333, synth.NORM, 0, 1, 0)],
+                                          dtype=segs.dtype)])
+    n = synth.segments_numel(segs)
+    assert n > 2 ** 31 and n % 8 == 5
+    free, _ = torch.cuda.mem_get_info()
+    need = 6 * 4 * n + 2 * n
+    if free < need + (4 << 30):
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of free HBM")
+    M, p, r = 2, 0, 1
+    cfg = cfg_for(B, tau=1)
+    rep = EmulatedReplicas(cfg, M, n)
+    A_d = synth.dev_init(torch.empty(n, device=DEV), segs, p)
+    Acopies = [A_d, A_d.clone()]
+    v_d = [torch.zeros(n, device=DEV) for _ in range(M)]
+    th_d = []
+    for m in range(M):
+        th = A_d.clone()
+        synth.dev_apply_window(th, segs, p, m, r)
+        th_d.append(th)
+    rep.quantize_all(p, 10, th_d, Acopies)
+    for m in range(M):
+        synth.dev_apply_drift(th_d[m], segs, p, m, r)
+    rep.merge_all(p, 11, th_d, Acopies, v_d)
+    torch.cuda.synchronize()
+    nb = -(-n // B)
+    rng = np.random.default_rng(31)
+    edges = [2 ** 30 // B - 1, 2 ** 30 // B, 2 ** 31 // B - 1, 2 ** 31 // B]
+    blocks = sorted(set([0, nb - 1] + edges + list(rng.integers(0, nb, 16))))
+    soff = sd.sd_payload_scales_offset(n)
+    gat = rep.gather
+    for b in blocks:
+        lo, hi = b * B, min(n, (b + 1) * B)
+        A0 = synth.host_init(segs, p, lo, hi)
+        sends = [synth.host_apply_window(A0.copy(), segs, p, m, r, i0=lo) for m in range(M)]
+        merges = [synth.host_apply_drift(x.copy(), segs, p, m, r, i0=lo) for m, x in enumerate(sends)]
+        Ao, vo = A0.copy(), np.zeros(hi - lo, np.float32)
+        st, g_o = oracle.round_(sends, merges, Ao, vo, B=B)
+        assert st == 0
+        pb_o = oracle.payload_bytes(hi - lo, B)
+        so = oracle.scales_offset(hi - lo)
+        for m in range(M):
+            base = m * rep.pb
+            got_codes = gat[base + lo // 2: base + (hi + 1) // 2].cpu().numpy()
+            assert np.array_equal(got_codes, g_o[m * pb_o: m * pb_o + (hi - lo + 1) // 2]), f"block {b} codes"
+            got_s = gat[base + soff + 4 * b: base + soff + 4 * b + 4].cpu().numpy()
+            assert np.array_equal(got_s, g_o[m * pb_o + so: m * pb_o + so + 4]), f"block {b} scale"
+            assert_same(Acopies[m][lo:hi], Ao, f"block {b} anchor")
+            assert_same(v_d[m][lo:hi], vo, f"block {b} momentum")
+            assert_same(th_d[m][lo:hi], merges[m], f"block {b} theta")
+    rep.close()
+
+
 def test_gather_alloc_single_gpu_and_free_errors():
     """sd_gather_alloc without a communicator: plain device memory, usable by
     the round; freeing a pointer it did not allocate is SD_ERR_ARG."""
