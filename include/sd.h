@@ -261,7 +261,9 @@ sd_status sd_fragment_wait(sd_ctx* ctx, int32_t p, int64_t t, sd_stream stream);
  * ascending replica order, Nesterov on (anchor, momentum), alpha-merge into
  * theta (the live parameters after tau inner steps).  p must be received at
  * t (send step + tau, or the flush at T).  If any payload is poisoned or
- * malformed, nothing is written (identically on every replica). */
+ * malformed, nothing is written (identically on every replica).  An NCCL
+ * async error already reported by the communicator fails the call with
+ * SD_ERR_NCCL before anything is enqueued. */
 sd_status sd_merge(sd_ctx* ctx, int32_t p, int64_t t, const void* gather_buf, float* theta,
                    float* anchor, float* momentum, int64_t n, sd_stream stream);
 

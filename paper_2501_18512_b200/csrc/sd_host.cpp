@@ -807,6 +807,13 @@ sd_status do_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")) ||
                 (st = check_ptr(c, momentum, 32, "momentum"))))
     return st;
+  if (c->comm && !f.push) {  // a failed gather must not be merged (polled here and in sd_check)
+    ncclResult_t ar = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError(c->comm, &ar);
+    if (r != ncclSuccess || ar != ncclSuccess)
+      return ctx_fail(c, SD_ERR_NCCL, "fragment %d: NCCL async error before the merge: %s", p,
+                      ncclGetErrorString(r != ncclSuccess ? r : ar));
+  }
   const sdk::Payload pl = payload_of(&c->cfg, n);
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
