@@ -1,5 +1,7 @@
 """One 1B-fragment round for M = 2, 4, 8 replicas emulated on one GPU (for ncu
-captures of k_apply<M>): quantize all M slots, then replica 0's apply."""
+captures of k_apply<M>): quantize all M slots, then the M applies; replica 0's
+apply of the second round runs inside an NVTX range "capture", so
+`ncu --nvtx --nvtx-include "capture/"` captures exactly one launch per M."""
 import os
 import sys
 
@@ -27,7 +29,12 @@ for M in (2, 4, 8):
         th.append(x)
     for r in range(2):
         rep.quantize_all(0, 100, th, [A] * M)
-        rep.merge_all(0, 105, th, [A] * M, [v] * M)
+        for m in range(M):  # the second round's apply of replica 0 is the one ncu captures (NVTX range)
+            if r == 1 and m == 0:
+                torch.cuda.nvtx.range_push("capture")
+            rep.ctx[m].sd_merge(0, 105, rep.gather, th[m], A, v, n)
+            if r == 1 and m == 0:
+                torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     rep.close()
     del th

@@ -8,4 +8,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_quantize|k
 $CMD > gpurun_out/plain2_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_apply|k_quantize" -s 6 -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 python scripts/emulated_apply.py > gpurun_out/emu_$TAG.log 2>&1 && \
-ncu --set full --clock-control none -k regex:"k_apply" -s 2 -c 100 -o gpurun_out/prof_emu_$TAG python scripts/emulated_apply.py > gpurun_out/ncu_emu_$TAG.log 2>&1; echo "ncu emu rc=$?"
+ncu --set full --clock-control none --nvtx --nvtx-include "capture/" -k regex:"k_apply" -o gpurun_out/prof_emu_$TAG python scripts/emulated_apply.py > gpurun_out/ncu_emu_$TAG.log 2>&1; echo "ncu emu rc=$?"
