@@ -78,3 +78,25 @@ def test_fsdp_composition_two_replicas_two_shards():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "OK" in out, out[-3000:]
+
+
+def _run_fullsize(nproc, gather):
+    env = dict(os.environ, SD_TEST_GATHER=gather)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(HERE, "dist_fullsize_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    return r.returncode, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("nproc,gather", [(2, "auto"), (4, "auto"), (4, "pull")])
+def test_full_size_1b_fragment_multi_rank(nproc, gather):
+    """BASELINE.json's 1B fragment (n = 151,007,616) on 2 and 4 ranks in the
+    bench's configuration (AUTO gather: copy engines at tau = 5) and with the
+    fused pull: sampled blocks equal the oracle, A and v bit-identical on
+    every rank over the whole fragment, every gathered slot equals its
+    owner's payload."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    rc, out = _run_fullsize(nproc, gather)
+    assert rc == 0 and "OK" in out, out[-3000:]
