@@ -314,3 +314,34 @@ def test_adamw_vs_torch():
         assert np.allclose(st["exp_avg"].numpy(), m, rtol=1e-5, atol=1e-9)
         assert np.allclose(st["exp_avg_sq"].numpy(), v, rtol=1e-5, atol=1e-12)
         assert np.max(np.abs(p.detach().numpy() - th)) <= 1e-6 * max(1.0, float(np.max(np.abs(th))))
+
+
+@pytest.mark.parametrize("M", [1, 2, 4])
+def test_apply_single_replica_fedavg_and_poison(M):
+    """or_apply (one replica's receive side on a given gather buffer):
+    lr = 1, mu = 0, alpha = 0.5 on grid -> the anchor is the plain average
+    of the M senders' parameters (FedAvg) and theta = (theta + A) / 2
+    (P:137), bit-exact; the momentum is the mean outer gradient
+    (v = 0 + g).  A poisoned slot leaves A, v, theta untouched and
+    returns nonzero."""
+    rng = np.random.default_rng(300 + M)
+    n, B = 2048 + 77, 1024
+    A, _, _ = on_grid(rng, n, B)
+    sends = [(A - on_grid(rng, n, B)[1]).astype(np.float32) for _ in range(M)]
+    pb = oracle.payload_bytes(n, B)
+    gather = np.concatenate([oracle.quantize(s, A, B)[0] for s in sends])
+    assert gather.size == M * pb
+    theta = (A + np.float32(2.0 ** -10)).astype(np.float32)
+    Aw, v, th = A.copy(), np.zeros(n, np.float32), theta.copy()
+    st = oracle.apply(gather, M, n, B, Aw, v, th, lr=1.0, mu=0.0, alpha=0.5)
+    assert st == 0
+    avg = np.mean(np.stack(sends).astype(np.float64), axis=0)
+    assert np.array_equal(Aw.astype(np.float64), avg)
+    assert np.array_equal(v.astype(np.float64), A.astype(np.float64) - avg)
+    assert np.array_equal(th.astype(np.float64), 0.5 * theta.astype(np.float64) + 0.5 * avg)
+    bad = [s.copy() for s in sends]
+    bad[-1][n // 2] = np.nan
+    gather = np.concatenate([oracle.quantize(s, A, B)[0] for s in bad])
+    Aw, v, th = A.copy(), np.zeros(n, np.float32), theta.copy()
+    assert oracle.apply(gather, M, n, B, Aw, v, th) != 0
+    assert np.array_equal(bits(Aw), bits(A)) and not v.any() and np.array_equal(bits(th), bits(theta))
