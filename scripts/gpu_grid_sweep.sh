@@ -1,3 +1,4 @@
+# grid-size sweep: bench.py at several SD_BLOCKS_PER_SM caps (CTAs per SM) on 1 GPU -> gpurun_out/grid_*.json
 mkdir -p gpurun_out
 for k in ${KS:-8 16 32 64 100000}; do
   SD_BLOCKS_PER_SM=$k python bench.py --steps 64 --warmup 8 --no-e2e --no-cpu-baseline > gpurun_out/grid_$k.json 2>/dev/null

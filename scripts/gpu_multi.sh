@@ -1,3 +1,4 @@
+# N GPUs ($1, default 2): multi-GPU tests, then bench.py under torchrun; prints value, roofline, overlap, clocks
 mkdir -p gpurun_out
 N=${1:-2}
 nvidia-smi topo -m | head -8

@@ -1,3 +1,4 @@
+# N GPUs ($1): bench.py per gather mode (GATHERS env, default ce push pull) -> gpurun_out/bench_n$N_<mode>.json
 mkdir -p gpurun_out
 N=${1:-2}
 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/pytest_push_$N.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_push_$N.log
