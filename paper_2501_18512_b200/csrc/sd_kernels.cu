@@ -854,6 +854,154 @@ __global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, Adam
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_apply_tma: k_apply with a tile's A, v, theta and M code chunks staged
+// through shared memory by 1-D bulk copies (cp.async.bulk) in a
+// kAStages-deep mbarrier ring: one producer warp, kAW consumer warps (two
+// 256-element rows each), results stored directly with 256-bit stores.
+// Persistent grid (one CTA per SM), whole tiles only -- launch_apply hands
+// the rest to k_apply.  The north star's "staged through shared memory/TMA"
+// design, kept as a measured alternative (SD_APPLY_TMA=1); same arithmetic
+// (decode8 + ascending-m sum + outer_step), so bit-identical to k_apply.
+// ---------------------------------------------------------------------------
+#ifndef SD_ATMA_STAGES
+#define SD_ATMA_STAGES 2  // best of the measured configurations (profiles/atma_ab_r1.txt)
+#endif
+#ifndef SD_ATMA_CTAS
+#define SD_ATMA_CTAS 1  // CTAs per SM
+#endif
+constexpr int kAW = 8;                  // consumer warps
+constexpr int kATile = kAW * 512;       // elements per tile
+constexpr int kAStages = SD_ATMA_STAGES;
+constexpr int kATmaThreads = 32 * (kAW + 1);
+template <int kM>
+struct ApplyTmaLayout {
+  static constexpr int kArr = 4 * kATile;                      // bytes of A (or v, theta) per stage
+  static constexpr int kCodes = kATile / 2;                    // code bytes per slot per stage
+  static constexpr int kStage = 3 * kArr + kM * kCodes;
+  static constexpr int kSmem = kAStages * kStage + 2 * kAStages * 8;
+};
+
+template <int kM>
+__global__ void __launch_bounds__(kATmaThreads, SD_ATMA_CTAS) k_apply_tma(AArgs p, int64_t ntiles) {
+  using L = ApplyTmaLayout<kM>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAStages * L::kStage);
+  uint64_t* empty = full + kAStages;
+  __shared__ int skip;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint8_t* gbase = p.gather;
+  const size_t gstride = p.pb;
+  if (threadIdx.x == 0) {
+    unsigned long long fb = ~0ull;
+    int badmagic = 0;
+    for (int m = 0; m < kM; ++m) {
+      const uint8_t* tr = gbase + (size_t)m * gstride + p.trailer_off;
+      if (*reinterpret_cast<const uint32_t*>(tr) != kMagic) badmagic = 1;
+      const unsigned long long f = *reinterpret_cast<const unsigned long long*>(tr + 8);
+      fb = f < fb ? f : fb;
+    }
+    skip = badmagic || fb != ~0ull;
+    if (skip && blockIdx.x == 0 && p.status) {
+      volatile unsigned long long* st = p.status;
+      st[0] = fb;
+      st[1] = badmagic ? 2ull : 1ull;
+    }
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kAW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (skip) return;
+  if (warp == 0) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kAStages;
+        const uint32_t ph = (uint32_t)(it / kAStages) & 1u;
+        mbar_wait(&empty[st], ph ^ 1u);
+        mbar_expect_tx(&full[st], L::kStage);
+        uint8_t* sb = smem + st * L::kStage;
+        const int64_t e0 = tile * kATile;
+        bulk_g2s(sb, p.A + e0, L::kArr, &full[st]);
+        bulk_g2s(sb + L::kArr, p.v + e0, L::kArr, &full[st]);
+        bulk_g2s(sb + 2 * L::kArr, p.theta + e0, L::kArr, &full[st]);
+#pragma unroll
+        for (int m = 0; m < kM; ++m)
+          bulk_g2s(sb + 3 * L::kArr + m * L::kCodes, gbase + (size_t)m * gstride + e0 / 2, L::kCodes, &full[st]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kAStages;
+    const uint32_t ph = (uint32_t)(it / kAStages) & 1u;
+    mbar_wait(&full[st], ph);
+    const uint8_t* sb = smem + st * L::kStage;
+#pragma unroll 1
+    for (int r = 0; r < 2; ++r) {  // one 256-element row at a time: 24 floats + M code words live
+      const int le = cw * 512 + r * 256 + 8 * lane;
+      const float* sa = reinterpret_cast<const float*>(sb) + le;
+      const float* sv = reinterpret_cast<const float*>(sb + L::kArr) + le;
+      const float* stt = reinterpret_cast<const float*>(sb + 2 * L::kArr) + le;
+      f8 a, w, t;
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(sa + j);
+        const float4 y = *reinterpret_cast<const float4*>(sv + j);
+        const float4 z = *reinterpret_cast<const float4*>(stt + j);
+        a.v[j] = x.x; a.v[j + 1] = x.y; a.v[j + 2] = x.z; a.v[j + 3] = x.w;
+        w.v[j] = y.x; w.v[j + 1] = y.y; w.v[j + 2] = y.z; w.v[j + 3] = y.w;
+        t.v[j] = z.x; t.v[j + 1] = z.y; t.v[j + 2] = z.z; t.v[j + 3] = z.w;
+      }
+      uint32_t code[kM];
+#pragma unroll
+      for (int m = 0; m < kM; ++m) code[m] = *reinterpret_cast<const uint32_t*>(sb + 3 * L::kArr + m * L::kCodes + le / 2);
+      const int64_t e = tile * kATile + le;
+      const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
+      float S[8];
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const float sc = __ldg(reinterpret_cast<const float*>(gbase + (size_t)m * gstride + p.scales_off) + blk);
+        float q[8];
+        decode8(code[m], sc, q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) S[j] = (m == 0) ? q[j] : __fadd_rn(S[j], q[j]);  // ascending m
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) outer_step(S[j], a.v[j], w.v[j], t.v[j], p);
+      st8(p.A + e, a);
+      st8(p.v + e, w);
+      st8(p.theta + e, t);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // the stage may be refilled
+  }
+}
+
+bool use_tma_apply() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_APPLY_TMA");
+    v = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int kM>
+void launch_apply_tma(const AArgs& p, int64_t ntiles, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_apply_tma<kM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ApplyTmaLayout<kM>::kSmem);
+    attr = true;
+  }
+  k_apply_tma<kM><<<grid, kATmaThreads, ApplyTmaLayout<kM>::kSmem, st>>>(p, ntiles);
+}
+
 int ilog2_or_neg(int32_t B) {
   if (B <= 0) return -1;
   int l = 0;
@@ -1057,7 +1205,38 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.half_off = p.pull ? pull->half_off : 0;
   AdamArgs h{};
   if (inner) h = make_adam(theta, inner->grad, inner->m, inner->v, pl.n, inner->hp);
-  const int64_t items = (pl.n >> 3) > 0 ? (pl.n >> 3) : 1;
+  int launched = 0;
+  // SD_APPLY_TMA=1: whole tiles through the bulk-copy pipeline (local slots,
+  // no inner step, B a divisor of the tile), the rest through k_apply below
+  const int64_t ntiles = (use_tma_apply() && !inner && !p.pull && (M == 1 || M == 2 || M == 4 || M == 8) &&
+                          (pl.B == 0 || (pl.B >= 256 && pl.B <= kATile)))
+                             ? pl.n / kATile
+                             : 0;
+  if (ntiles > 0) {
+#ifdef SD_ATMA_ONESHOT
+    const int64_t cap = ntiles;  // one CTA per tile
+#else
+    const int64_t cap = (int64_t)num_sms * SD_ATMA_CTAS;
+#endif
+    const int g = (int)(ntiles < cap ? ntiles : cap);
+    switch (M) {
+      case 1: launch_apply_tma<1>(p, ntiles, g, st); break;
+      case 2: launch_apply_tma<2>(p, ntiles, g, st); break;
+      case 4: launch_apply_tma<4>(p, ntiles, g, st); break;
+      default: launch_apply_tma<8>(p, ntiles, g, st); break;
+    }
+    ++launched;
+    const int64_t off = ntiles * kATile;  // a multiple of B: shift every stream to the rest
+    p.A += off;
+    p.v += off;
+    p.theta += off;
+    p.n -= off;
+    p.gather += off / 2;
+    p.scales_off = p.scales_off - (size_t)(off / 2) + (p.lgB < 0 ? 0 : 4 * (size_t)(off >> p.lgB));
+    p.trailer_off -= (size_t)(off / 2);
+    if (p.n == 0) return cudaGetLastError() == cudaSuccess ? launched : -1;
+  }
+  const int64_t items = (p.n >> 3) > 0 ? (p.n >> 3) : 1;
 #define SD_APPLY_CASE(KM)                                                                                         \
   if (inner)                                                                                                      \
     k_apply<KM, true><<<grid_for(k_apply<KM, true>, num_sms, items, kThreads), kThreads, 0, st>>>(p, h);          \
@@ -1071,7 +1250,7 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
     default: SD_APPLY_CASE(0) break;
   }
 #undef SD_APPLY_CASE
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return cudaGetLastError() == cudaSuccess ? launched + 1 : -1;
 }
 
 }  // namespace sdk
