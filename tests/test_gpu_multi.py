@@ -100,3 +100,20 @@ def test_full_size_1b_fragment_multi_rank(nproc, gather):
         pytest.skip(f"needs {nproc} GPUs")
     rc, out = _run_fullsize(nproc, gather)
     assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
+def test_fused_inner_steps_two_ranks_bit_exact(gather):
+    """sd_inner_adamw_quantize / sd_inner_adamw / sd_inner_adamw_merge on 2
+    NCCL ranks in each gather mode (push: the fused AdamW + quantize kernel
+    also stores into the peers; pull: the fused AdamW + merge kernel reads the
+    peers' payloads): theta, AdamW moments, anchor, momentum and payloads
+    bit-identical to or_adamw + or_round after every round."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = dict(os.environ, SD_TEST_GATHER=gather)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_fused_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "OK" in out, out[-3000:]
