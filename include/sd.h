@@ -36,6 +36,11 @@
  *  - One sd_ctx per replica (= per GPU process), used from one host thread
  *    in program order.  The schedule functions are pure and thread-safe.
  *  - Layout: a fragment is one contiguous fp32 slab of n elements (AMB-18).
+ *  - Environment (read once per process; measurement switches, results are
+ *    bit-identical either way): SD_QUANTIZE_TMA=1 / SD_APPLY_TMA=1 select the
+ *    bulk-copy (TMA) staged quantize / apply kernels, measured slower than the
+ *    default direct-load kernels; SD_BLOCKS_PER_SM=k caps the
+ *    grids at k CTAs per SM.
  */
 #ifndef SD_H_
 #define SD_H_
