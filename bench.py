@@ -62,9 +62,10 @@ def parse():
     ap.add_argument("--serial", action="store_true", help="no send/receive pipelining across fragments")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as a CUDA graph (auto: single GPU, L2-resident small configs)")
-    ap.add_argument("--gather", choices=["auto", "ce", "push", "pull"], default="auto",
+    ap.add_argument("--gather", choices=["auto", "ce", "push", "pull", "mc"], default="auto",
                     help="all-gather: NCCL copy engines (ce), fused into the quantize kernel (push) or into "
-                         "the merge kernel (pull), or libsd's choice (auto)")
+                         "the merge kernel (pull), one copy-engine write through the NVLS multicast alias (mc), "
+                         "or libsd's choice (auto)")
     return ap.parse_args()
 
 
@@ -351,7 +352,8 @@ def main():
         theta.append(th)
     sync = FragmentSync(cfg, n, rank, world, local,
                         gather_mode={"auto": sd.SD_GATHER_AUTO, "ce": sd.SD_GATHER_COPY_ENGINE,
-                                     "push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}[args.gather])
+                                     "push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL,
+                                     "mc": sd.SD_GATHER_MULTICAST}[args.gather])
     torch.cuda.synchronize()
 
     K, W = args.steps, max(1, args.warmup)
@@ -626,7 +628,9 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
             "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n],
-                           gather=("fused into k_apply: NVLink loads of the peers' payloads + flag handshake"
+                           gather=("copy engine writes each payload once through the NVLS multicast alias "
+                                   "(NVSwitch replicates), flag handshake" if args.gather == "mc" else
+                                   "fused into k_apply: NVLink loads of the peers' payloads + flag handshake"
                                    if (args.gather == "pull" or (args.gather == "auto" and cfg.tau == 0 and
                                                                  world in (4, 8))) else
                                    "fused into k_quantize: NVLink stores to the peers' symmetric buffers + "

@@ -176,9 +176,17 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  *                         block-receive is an acquire-wait on the peers'
  *                         flags.  Buffers hold two rounds (alternating by
  *                         round id), so no rendezvous is needed.
+ *  SD_GATHER_MULTICAST    zero-SM, one HBM read per payload: the quantize
+ *                         writes a staging slot; the sync has the copy
+ *                         engine write it once through the gather window's
+ *                         NVLS multicast alias (NCCL device API, LSA-team
+ *                         multimem), NVSwitch delivers it into every rank's
+ *                         slot, then a one-thread kernel release-signals the
+ *                         round flag as in PUSH.  Falls back to COPY_ENGINE
+ *                         where the system has no multicast.
  * With caller-owned buffers or without a communicator the mode is ignored.
- * In PUSH and PULL modes a gather buffer must serve a single fragment (its
- * round ids count that fragment's sends). */
+ * In PUSH, PULL and MULTICAST modes a gather buffer must serve a single
+ * fragment (its round ids count that fragment's sends). */
 #define SD_GATHER_COPY_ENGINE 0
 #define SD_GATHER_PUSH 1
 #define SD_GATHER_AUTO 2 /* default: COPY_ENGINE when tau >= 1 (hidden behind later work); with tau == 0
@@ -186,6 +194,7 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
 #define SD_GATHER_PULL 3 /* fused into the apply: the quantize writes locally and signals; the merge
                             kernel reads the peers' payloads from their buffers over NVLink (no HBM
                             staging of the M payloads); M in {2, 4, 8}, else COPY_ENGINE */
+#define SD_GATHER_MULTICAST 4
 sd_status sd_set_gather_mode(sd_ctx* ctx, int32_t mode);
 
 /* Address of the M payloads of fragment p's most recent round inside

@@ -124,6 +124,7 @@ struct Inflight {
   const void* gather = nullptr;
   bool push = false;      // two-round symmetric buffer with round flags (PUSH or PULL mode)
   bool pull = false;      // PULL: the apply reads the peers' slots over NVLink
+  bool mc = false;        // MULTICAST: the sync copies the staged payload through the multicast alias
   bool waited = false;    // push mode: the block-receive wait kernel was issued
   size_t half_off = 0;    // push mode: byte offset of this round's half
   uint64_t seq = 0;       // push mode: round id published in the peers' flags
@@ -138,6 +139,8 @@ struct GatherBuf {
   bool nccl = false;
   bool push = false;   // two-round layout: halves (round parity) of M payloads + M round flags (PUSH/PULL)
   bool pull = false;   // PULL mode: peers' payloads stay in the peers' buffers, read by the apply
+  bool mc = false;     // MULTICAST mode: staging slot at 2*half, copied through the multicast alias
+  uint8_t* mc_base = nullptr;  // multicast address of byte 0 of the buffer
   size_t half = 0;     // bytes per half
   size_t pb = 0;       // payload bytes
 };
@@ -149,6 +152,8 @@ struct sd_ctx {
   std::vector<uint64_t> round_seq;  // push mode: sends of each fragment so far (round id, same on every rank)
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
+  sdk::McState* mc = nullptr;  // NCCL device communicator with the multimem handle (MULTICAST mode)
+  int mc_state = 0;            // 0 not tried, 1 available, -1 unavailable
   cudaStream_t comm_stream = nullptr;
   cudaStream_t copy_stream = nullptr;               // outer-state offload (NEXT-3)
   std::vector<cudaEvent_t> ready, done;
@@ -404,11 +409,19 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   if (mode == SD_GATHER_AUTO)
     mode = c->cfg.tau > 0 ? SD_GATHER_COPY_ENGINE : ((c->M == 4 || c->M == 8) ? SD_GATHER_PULL : SD_GATHER_PUSH);
   if (mode == SD_GATHER_PULL && !(c->M == 2 || c->M == 4 || c->M == 8)) mode = SD_GATHER_COPY_ENGINE;
-  b.push = c->comm && (mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL);
+  if (mode == SD_GATHER_MULTICAST && c->comm && c->mc_state == 0) {
+    // collective: every rank allocates its gather buffers in the same order and mode
+    const int r = sdk::mc_create(c->comm, &c->mc);
+    if (r < 0) return ctx_fail(c, SD_ERR_NCCL, "ncclDevCommCreate(lsaMultimem) failed");
+    c->mc_state = r == 1 ? 1 : -1;
+  }
+  if (mode == SD_GATHER_MULTICAST && c->mc_state != 1) mode = SD_GATHER_COPY_ENGINE;  // no NVLS here
+  b.push = c->comm && (mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL || mode == SD_GATHER_MULTICAST);
   b.pull = b.push && mode == SD_GATHER_PULL;
+  b.mc = b.push && mode == SD_GATHER_MULTICAST;
   if (b.push) {
     b.half = (size_t)align_up((int64_t)(b.pb * (size_t)c->M) + 256, 256);
-    b.bytes = (size_t)align_up((int64_t)(2 * b.half), 2 << 20);
+    b.bytes = (size_t)align_up((int64_t)(2 * b.half + (b.mc ? b.pb : 0)), 2 << 20);
   } else {
     b.bytes = (size_t)align_up((int64_t)(b.pb * (size_t)c->M), 2 << 20);
   }
@@ -432,6 +445,10 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
       return ctx_fail(c, SD_ERR_NCCL, "ncclCommWindowRegister(%zu): %s", b.bytes, ncclGetErrorString(r));
     }
     b.nccl = true;
+    if (b.mc && sdk::mc_base(c->mc, b.win, &b.mc_base, c->comm_stream) < 0) {
+      release(c, b);
+      return ctx_fail(c, SD_ERR_CUDA, "multicast address of the gather window: %s", cudaGetErrorString(cudaGetLastError()));
+    }
   } else {
     SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
   }
@@ -468,8 +485,10 @@ sd_status sd_gather_payloads(sd_ctx* c, int32_t p, const void* gather_buf, const
 
 sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
-  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO && mode != SD_GATHER_PULL)
-    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, _PUSH, _PULL or _AUTO", mode);
+  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO && mode != SD_GATHER_PULL &&
+      mode != SD_GATHER_MULTICAST)
+    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, _PUSH, _PULL, _MULTICAST or _AUTO",
+                    mode);
   for (const Inflight& f : c->fl)
     if (f.state != IDLE) return ctx_fail(c, SD_ERR_STATE, "gather mode changed while a fragment is in flight");
   c->gather_mode = mode;
@@ -563,6 +582,7 @@ struct PushRound {
   size_t half_off = 0;
   uint64_t seq = 0;
   bool pull = false;
+  bool mc = false;
   sdk::Push push;
 };
 
@@ -576,13 +596,14 @@ sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk:
   r->seq = c->round_seq[p] + 1;  // this send's round id (identical on every rank: same call sequence)
   r->buf = b;
   r->half_off = (size_t)(r->seq & 1) * b->half;
-  if (!b->pull) {  // PUSH: the quantize stores into the peers' buffers
+  if (!b->pull && !b->mc) {  // PUSH: the quantize stores into the peers' buffers
     r->push.win = b->win;
     r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
     r->push.rank = c->rank;
     r->push.M = c->M;
   }
   r->pull = b->pull;
+  r->mc = b->mc;
   return SD_OK;
 }
 
@@ -590,6 +611,7 @@ sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk:
 // for a pending outer-state prefetch and the trailer's first_bad is reset.
 uint8_t* local_slot(sd_ctx* c, void* slot_out, const PushRound& pr, const sdk::Payload& pl) {
   if (!pr.buf) return static_cast<uint8_t*>(slot_out);
+  if (pr.mc) return static_cast<uint8_t*>(pr.buf->ptr) + 2 * pr.buf->half;  // staging slot
   return static_cast<uint8_t*>(pr.buf->ptr) + pr.half_off + (size_t)c->rank * pl.bytes;
 }
 
@@ -618,7 +640,9 @@ sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const 
 
 sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, const PushRound& pr,
                    const sdk::Payload& pl, cudaStream_t s) {
-  if (pr.buf) {  // fused all-gather: publish this round to the peers
+  if (pr.buf && pr.mc) {  // multicast: the sync copies and signals
+    c->round_seq[p] = pr.seq;
+  } else if (pr.buf) {  // fused all-gather: publish this round to the peers
     sdk::Push sig = pr.push;  // the signal reaches every peer in both modes
     sig.win = pr.buf->win;
     sig.win_off = pr.half_off + (size_t)c->rank * pl.bytes;
@@ -636,6 +660,7 @@ sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, c
   c->fl[p].slot = slot_out;
   c->fl[p].push = pr.buf != nullptr;
   c->fl[p].pull = pr.pull;
+  c->fl[p].mc = pr.mc;
   c->fl[p].waited = false;
   c->fl[p].half_off = pr.half_off;
   c->fl[p].seq = pr.seq;
@@ -737,7 +762,19 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
                     c->rank, pl.bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
-  if (f.push) {  // the payloads were pushed by the quantize: nothing to transfer
+  if (f.mc) {  // one copy-engine write through the multicast alias reaches every rank's slot
+    GatherBuf* b = find_buf(c, gather_buf);
+    if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: multicast gather buffer not found", p);
+    SD_CUDA(c, cudaEventRecord(c->ready[p], s));
+    SD_CUDA(c, cudaStreamWaitEvent(c->comm_stream, c->ready[p], 0));
+    SD_CUDA(c, cudaMemcpyAsync(b->mc_base + f.half_off + (size_t)c->rank * pl.bytes, static_cast<uint8_t*>(b->ptr) + 2 * b->half,
+                               pl.bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+    const int k = sdk::launch_flag_signal(b->win, f.half_off + (size_t)c->M * pl.bytes, c->rank, c->M, f.seq,
+                                          c->comm_stream);
+    if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_flag_signal launch");
+    g_launches += (uint64_t)k;
+    SD_CUDA(c, cudaEventRecord(c->done[p], c->comm_stream));
+  } else if (f.push) {  // the payloads were pushed by the quantize: nothing to transfer
     SD_CUDA(c, cudaEventRecord(c->done[p], s));
   } else if (c->comm) {
     SD_CUDA(c, cudaEventRecord(c->ready[p], s));
@@ -889,6 +926,10 @@ sd_status sd_finalize(sd_ctx* c) {
   if (!c->bufs.empty()) cudaDeviceSynchronize();
   for (GatherBuf& b : c->bufs) release(c, b);
   c->bufs.clear();
+  if (c->mc) {
+    sdk::mc_destroy(c->comm, c->mc);
+    c->mc = nullptr;
+  }
   if (c->comm) {
     ncclCommDestroy(c->comm);
     c->comm = nullptr;

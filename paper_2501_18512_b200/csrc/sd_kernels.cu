@@ -1123,6 +1123,69 @@ int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ---------------------------------------------------------------------------
+// Multicast gather support (NVLS through the NCCL device API).
+// ---------------------------------------------------------------------------
+struct McState {
+  ncclDevComm_t dc;
+  void** host_ptr = nullptr;  // mapped pinned word for mc_base
+};
+
+namespace {
+__global__ void k_mc_base(ncclWindow_t w, ncclMultimemHandle mm, void** out) {
+  *out = ncclGetMultimemPointer(w, 0, mm);
+}
+__global__ void k_flag_signal(ncclWindow_t w, size_t flags_off, int rank, int M, unsigned long long t) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int q = 0; q < M; ++q) {
+    if (q == rank) continue;
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(w, flags_off + 8 * (size_t)rank, q));
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(t) : "memory");
+  }
+}
+}  // namespace
+
+int mc_create(ncclComm_t comm, McState** out) {
+  *out = nullptr;
+  McState* s = new McState();
+  ncclDevCommRequirements_t req = {};
+  req.lsaMultimem = true;
+  if (ncclDevCommCreate(comm, &req, &s->dc) != ncclSuccess) {
+    delete s;
+    return -1;
+  }
+  if (s->dc.lsaMultimem.mcBasePtr == nullptr ||
+      cudaHostAlloc(reinterpret_cast<void**>(&s->host_ptr), sizeof(void*), cudaHostAllocMapped) != cudaSuccess) {
+    ncclDevCommDestroy(comm, &s->dc);
+    delete s;
+    return 0;
+  }
+  *out = s;
+  return 1;
+}
+
+void mc_destroy(ncclComm_t comm, McState* s) {
+  if (!s) return;
+  ncclDevCommDestroy(comm, &s->dc);
+  if (s->host_ptr) cudaFreeHost(s->host_ptr);
+  delete s;
+}
+
+int mc_base(McState* s, ncclWindow_t win, uint8_t** out, cudaStream_t st) {
+  void** dev = nullptr;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), s->host_ptr, 0) != cudaSuccess) return -1;
+  k_mc_base<<<1, 1, 0, st>>>(win, s->dc.lsaMultimem, dev);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  *out = static_cast<uint8_t*>(*reinterpret_cast<void* volatile*>(s->host_ptr));
+  return *out ? 1 : -1;
+}
+
+int launch_flag_signal(ncclWindow_t win, size_t flags_off, int rank, int M, uint64_t t, cudaStream_t st) {
+  k_flag_signal<<<1, 32, 0, st>>>(win, flags_off, rank, M, (unsigned long long)t);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
 int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
                      uint64_t timeout_ns, unsigned long long* status, cudaStream_t st) {
   k_push_wait<<<1, 32, 0, st>>>(flags, half, pl.bytes, pl.trailer_off, M, rank, (unsigned long long)t,

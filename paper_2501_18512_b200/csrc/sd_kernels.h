@@ -41,6 +41,23 @@ int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_
 int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
                      uint64_t timeout_ns, unsigned long long* status, cudaStream_t st);
 
+// Multicast gather (SD_GATHER_MULTICAST): the copy engine writes this rank's
+// payload once through the window's NVLS multicast alias and NVSwitch
+// delivers it to every rank's slot.  McState wraps the NCCL device
+// communicator that owns the LSA-team multimem handle.
+struct McState;
+// Collective (all ranks, same order).  Returns 1 and *out on success, 0 if the
+// system has no multicast (no NVLS), -1 on an NCCL error.
+int mc_create(ncclComm_t comm, McState** out);
+void mc_destroy(ncclComm_t comm, McState* s);
+// Device address of byte 0 of window `win` in the multicast space (the
+// alias is linear in the window offset).  Synchronizes `st`.
+int mc_base(McState* s, ncclWindow_t win, uint8_t** out, cudaStream_t st);
+// Release-store the round id t into flags[rank] of every peer (window offset
+// flags_off) after a system-scope fence: ordered after the stream's prior
+// work, i.e. after the multicast copy has landed everywhere.
+int launch_flag_signal(ncclWindow_t win, size_t flags_off, int rank, int M, uint64_t t, cudaStream_t st);
+
 // AdamW hyper-parameters with the host-side constants of the op order
 // (bias corrections in binary64 rounded once, DESIGN.md AMB-20).
 struct AdamHyper {

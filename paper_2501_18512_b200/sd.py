@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("SD_LIBSD") or os.path.join(_HERE, "libsd.so")  # over
 SD_ABI_VERSION = 1
 SD_UNIQUE_ID_BYTES = 128
 SD_PAYLOAD_MAGIC = 0x31304453
-SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH, SD_GATHER_AUTO, SD_GATHER_PULL = 0, 1, 2, 3
+SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH, SD_GATHER_AUTO, SD_GATHER_PULL, SD_GATHER_MULTICAST = 0, 1, 2, 3, 4
 
 SD_OK, SD_ERR_ARG, SD_ERR_CONFIG, SD_ERR_SCHEDULE, SD_ERR_STATE, SD_ERR_NONFINITE, SD_ERR_CUDA, SD_ERR_NCCL = range(8)
 STATUS_NAMES = {

@@ -60,7 +60,18 @@ def test_fused_pull_gather_two_ranks_bit_exact(B):
     assert rc == 0 and "OK" in out, out[-3000:]
 
 
-@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
+@pytest.mark.parametrize("B", [1024, 0])
+def test_multicast_gather_two_ranks_bit_exact(B):
+    """SD_GATHER_MULTICAST: one copy-engine write per payload through the
+    NVLS multicast alias reaches every rank's slot, then the round-flag
+    handshake; 5 rounds = both buffer halves, repeated steps"""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, B, gather="mc")
+    assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull", "mc"])
 def test_nccl_allgather_four_ranks_bit_exact(gather):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
@@ -89,7 +100,7 @@ def _run_fullsize(nproc, gather):
     return r.returncode, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("nproc,gather", [(2, "auto"), (4, "auto"), (4, "pull")])
+@pytest.mark.parametrize("nproc,gather", [(2, "auto"), (4, "auto"), (4, "pull"), (4, "mc")])
 def test_full_size_1b_fragment_multi_rank(nproc, gather):
     """BASELINE.json's 1B fragment (n = 151,007,616) on 2 and 4 ranks in the
     bench's configuration (AUTO gather: copy engines at tau = 5) and with the
@@ -102,7 +113,7 @@ def test_full_size_1b_fragment_multi_rank(nproc, gather):
     assert rc == 0 and "OK" in out, out[-3000:]
 
 
-@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
+@pytest.mark.parametrize("gather", ["ce", "push", "pull", "mc"])
 def test_fused_inner_steps_two_ranks_bit_exact(gather):
     """sd_inner_adamw_quantize / sd_inner_adamw / sd_inner_adamw_merge on 2
     NCCL ranks in each gather mode (push: the fused AdamW + quantize kernel
