@@ -628,7 +628,8 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-based generator, synth/; Chinchilla-shaped fragments)",
             "config": dict(workload_config(wl, B, world), fragments=[int(x) for x in n],
-                           gather=("copy engine writes each payload once through the NVLS multicast alias "
+                           gather=("none (M = 1: no collective)" if world == 1 else
+                                   "copy engine writes each payload once through the NVLS multicast alias "
                                    "(NVSwitch replicates), flag handshake" if args.gather == "mc" else
                                    "fused into k_apply: NVLink loads of the peers' payloads + flag handshake"
                                    if (args.gather == "pull" or (args.gather == "auto" and cfg.tau == 0 and
