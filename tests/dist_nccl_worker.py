@@ -30,7 +30,9 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     segs = synth.fragment_segments(96, [0, 4], with_embed=True, vocab=333)
     n = synth.segments_numel(segs)
-    cfg = sd.sd_config_default(8, 2, 40, tau=3, scale_block=B)  # P = 4 fragments, H = 40
+    # per-replica tau: SD_TEST_TAU_PER_RANK=1 gives rank m tau = 1 + 2m
+    tau = 1 + 2 * rank if os.environ.get("SD_TEST_TAU_PER_RANK") == "1" else 3
+    cfg = sd.sd_config_default(8, 2, 40, tau=tau, scale_block=B)  # P = 4 fragments, H = 40
     P = sd.sd_fragment_count(cfg)
     p = 2
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)

@@ -23,8 +23,9 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False, gather="ce"):
-    env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather)
+def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False):
+    env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather,
+               SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
@@ -128,3 +129,14 @@ def test_fused_inner_steps_two_ranks_bit_exact(gather):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
+def test_per_replica_tau_two_ranks_bit_exact(gather):
+    """Heterogeneous overlap: rank m merges tau_m = 1 + 2m steps
+    after the shared send; every gather mode stays bit-exact (the round flags
+    and buffer halves do not assume the ranks receive together)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, 1024, gather=gather, tau_per_rank=True)
+    assert rc == 0 and "OK" in out, out[-3000:]
