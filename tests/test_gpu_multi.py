@@ -23,9 +23,9 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False):
+def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False):
     env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather,
-               SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0")
+               SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0", SD_TEST_POISON="1" if poison else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
@@ -139,4 +139,16 @@ def test_per_replica_tau_two_ranks_bit_exact(gather):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     rc, out = _run(2, 1024, gather=gather, tau_per_rank=True)
+    assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull", "mc"])
+def test_poisoned_round_skipped_on_every_rank(gather):
+    """A non-finite outer gradient on one rank (AMB-10): in every
+    gather mode the round is skipped on every rank -- A, v, theta unchanged,
+    identical to the oracle -- and sd_check reports SD_ERR_NONFINITE with the
+    index on every rank."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, 1024, gather=gather, poison=True)
     assert rc == 0 and "OK" in out, out[-3000:]
