@@ -184,6 +184,10 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  *                         slot, then a one-thread kernel release-signals the
  *                         round flag as in PUSH.  Falls back to COPY_ENGINE
  *                         where the system has no multicast.
+ * In PUSH, PULL and MULTICAST modes the block-receive waits at most 30 s
+ * (SD_WAIT_TIMEOUT_MS overrides) for each peer's round flag; on a timeout
+ * the round is skipped on this rank (A, v, theta untouched) and sd_check
+ * reports SD_ERR_STATE.
  * With caller-owned buffers or without a communicator the mode is ignored.
  * In PUSH, PULL and MULTICAST modes a gather buffer must serve a single
  * fragment (its round ids count that fragment's sends). */

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -791,7 +792,19 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
 }
 
 namespace {
-// push mode block-receive: one wait kernel per round (30 s bound per peer)
+// Bound of the block-receive spin on the peers' round flags: 30 s, or
+// SD_WAIT_TIMEOUT_MS (read once; tests shorten it to exercise the timeout).
+uint64_t wait_timeout_ns() {
+  static uint64_t ns = 0;
+  if (ns == 0) {
+    const char* e = getenv("SD_WAIT_TIMEOUT_MS");
+    const long long ms = e ? atoll(e) : 0;
+    ns = (ms > 0 ? (uint64_t)ms : 30000ull) * 1000000ull;
+  }
+  return ns;
+}
+
+// push mode block-receive: one wait kernel per round (bounded per peer)
 sd_status issue_push_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
   Inflight& f = c->fl[p];
   if (!f.push || f.waited) return SD_OK;
@@ -800,7 +813,7 @@ sd_status issue_push_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
   const sdk::Payload pl = payload_of(&c->cfg, f.n);
   uint8_t* half = static_cast<uint8_t*>(b->ptr) + f.half_off;
   const int k = sdk::launch_push_wait(reinterpret_cast<const unsigned long long*>(half + (size_t)c->M * pl.bytes),
-                                      half, pl, c->M, c->rank, f.seq, 30ull * 1000000000ull,
+                                      half, pl, c->M, c->rank, f.seq, wait_timeout_ns(),
                                       c->status_dev, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_wait launch");
   g_launches += (uint64_t)k;

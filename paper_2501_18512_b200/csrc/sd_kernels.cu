@@ -562,7 +562,11 @@ __global__ void k_push_wait(const unsigned long long* flags, uint8_t* half, size
     if (globaltimer_ns() - t0 > timeout_ns) break;
     __nanosleep(256);
   }
-  *reinterpret_cast<volatile uint32_t*>(half + (size_t)q * pb + trailer_off) = 0u;  // invalidate the slot
+  // invalidate the missing peer's local slot and this rank's own slot: the
+  // apply reads its own slot locally in every mode (the peers' slots are
+  // remote in pull mode), so a bad magic there makes it skip the round
+  *reinterpret_cast<volatile uint32_t*>(half + (size_t)q * pb + trailer_off) = 0u;
+  *reinterpret_cast<volatile uint32_t*>(half + (size_t)rank * pb + trailer_off) = 0u;
   if (status) {
     volatile unsigned long long* st = status;
     st[1] = 2ull;

@@ -152,3 +152,19 @@ def test_poisoned_round_skipped_on_every_rank(gather):
         pytest.skip("needs 2 GPUs")
     rc, out = _run(2, 1024, gather=gather, poison=True)
     assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["push", "pull", "mc"])
+def test_missing_peer_times_out_and_skips(gather):
+    """The block-receive of the flag-based modes is bounded: a peer that never
+    sends makes the wait time out (SD_WAIT_TIMEOUT_MS = 1500 here), the round
+    is skipped (A, v, theta untouched) and sd_check reports SD_ERR_STATE."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = dict(os.environ, SD_TEST_GATHER=gather, SD_WAIT_TIMEOUT_MS="1500")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(HERE, "dist_timeout_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "OK" in out, out[-3000:]
