@@ -747,7 +747,11 @@ template <int kM, bool kAdam>
 #ifndef SD_APPLY_MINB
 #define SD_APPLY_MINB 4  // <= 64 registers, no spills: M = 8 apply 1.03 vs 0.975 at 3 CTAs/SM (B200 A/B)
 #endif
-__global__ void __launch_bounds__(kThreads, SD_APPLY_MINB) k_apply(AArgs p, AdamArgs h) {
+#ifndef SD_APPLY_MINB_ADAM8
+#define SD_APPLY_MINB_ADAM8 3  // AdamW-fused M = 8 apply: spill-free at 80 registers, 1.060 vs 1.076 ms at 4 (profiles/fused_merge_r1.txt)
+#endif
+__global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_ADAM8 : SD_APPLY_MINB)
+    k_apply(AArgs p, AdamArgs h) {
   __shared__ int skip;
   const int M = kM > 0 ? kM : p.M;
   const uint8_t* gbase;
