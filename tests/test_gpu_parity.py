@@ -588,7 +588,7 @@ def test_no_writes_outside_buffers(n, B):
         c.sd_finalize()
 
 
-@pytest.mark.parametrize("M", [1, 2, 3])
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("poison", [False, True])
 def test_inner_adamw_merge_fused_bit_exact(M, poison):
     """The receive step's inner AdamW fused with the merge equals
