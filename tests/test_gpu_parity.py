@@ -517,7 +517,7 @@ def test_inner_adamw_bit_exact(n):
     ctx.sd_finalize()
 
 
-@pytest.mark.parametrize("B", [1024, 256, 0])
+@pytest.mark.parametrize("B", [1024, 512, 256, 0, 4096])
 @pytest.mark.parametrize("n", [1025, 64 * 1024 + 77])
 def test_inner_adamw_quantize_fused_bit_exact(n, B):
     """The fused last-inner-step + quantize equals AdamW then or_quantize."""
