@@ -48,6 +48,11 @@ def main():
     # SD_TEST_POISON=1: the last rank's theta holds a NaN at index 17 in the last round's send -> every
     # rank skips that round (A, v, theta unchanged) and sd_check reports SD_ERR_NONFINITE at 17 (AMB-10)
     poison = os.environ.get("SD_TEST_POISON") == "1"
+    # SD_TEST_OFFLOAD=1: A and v live in pinned host memory (NEXT-3); A, v on the device are staging
+    # buffers, scribbled before every prefetch, so the round can only be right if the copies are ordered
+    offload = os.environ.get("SD_TEST_OFFLOAD") == "1"
+    if offload:
+        hA, hv = A.cpu().pin_memory(), v.cpu().pin_memory()
     R = 5
 
     def same(a, b):  # bit-identical, NaN payloads aside
@@ -68,10 +73,20 @@ def main():
         synth.dev_apply_window(th, segs, p, rank, r)
         if bad and rank == world - 1:
             th[17] = float("nan")
+        if offload:
+            A.fill_(float("nan"))
+            v.fill_(-1.0)
+            fsync.ctx.sd_state_prefetch(p, hA, hv, A, v, n)
         fsync.send(p, t, th, A)
         synth.dev_apply_drift(th, segs, p, rank, r)      # tau overlapped inner steps
         assert p in sd.sd_fragment_schedule(cfg, t + cfg.tau)[1]
         fsync.receive(p, t + cfg.tau, th, A, v)
+        if offload:
+            fsync.ctx.sd_state_writeback(p, A, v, hA, hv, n)
+            fsync.ctx.sd_state_sync()
+            torch.cuda.synchronize()
+            A.copy_(hA)  # compare what the host store holds
+            v.copy_(hv)
         torch.cuda.synchronize()
         got = {}
         pb = fsync.payload[p]

@@ -23,9 +23,10 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False):
+def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False, offload=False):
     env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather,
-               SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0", SD_TEST_POISON="1" if poison else "0")
+               SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0", SD_TEST_POISON="1" if poison else "0",
+               SD_TEST_OFFLOAD="1" if offload else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
@@ -184,3 +185,15 @@ def test_soak_anchors_identical_across_ranks(gather):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "pull"])
+def test_offloaded_outer_state_two_ranks_bit_exact(gather):
+    """NEXT-3 with real NCCL: the outer state lives in pinned host memory,
+    prefetched before each send and written back after each merge on the copy
+    stream (device staging scribbled in between); the host store matches the
+    oracle after every round."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, 1024, gather=gather, offload=True)
+    assert rc == 0 and "OK" in out, out[-3000:]
