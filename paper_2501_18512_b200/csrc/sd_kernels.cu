@@ -508,8 +508,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_encode(QArgs a) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nfull = a.n >> 10;
-  for (int64_t c = warp; c < nfull; c += nwarps) encode_chunk<true>(a, c, lane);
-  if ((nfull << 10) < a.n && warp == nfull % nwarps) encode_chunk<false>(a, nfull, lane);
+  const int64_t nchunks = nfull + ((nfull << 10) < a.n ? 1 : 0);
+  // last chunk first: k_absmax streamed the fragment forward, so its tail is
+  // what the L2 still holds when this second pass starts
+  for (int64_t k = warp; k < nchunks; k += nwarps) {
+    const int64_t c = nchunks - 1 - k;
+    if (c < nfull) encode_chunk<true>(a, c, lane);
+    else encode_chunk<false>(a, c, lane);
+  }
   if (blockIdx.x == 0) write_tail(a);
 }
 
