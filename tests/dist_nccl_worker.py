@@ -28,7 +28,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    segs = synth.fragment_segments(96, [0, 4], with_embed=True, vocab=333)
+    tiny = os.environ.get("SD_TEST_TINY")  # SD_TEST_TINY=<n>: a flat fragment of n elements (0, 1, 7, ...)
+    segs = synth.flat_segments(int(tiny)) if tiny else synth.fragment_segments(96, [0, 4], with_embed=True, vocab=333)
     n = synth.segments_numel(segs)
     # per-replica tau: SD_TEST_TAU_PER_RANK=1 gives rank m tau = 1 + 2m
     tau = 1 + 2 * rank if os.environ.get("SD_TEST_TAU_PER_RANK") == "1" else 3

@@ -23,10 +23,12 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False, offload=False):
+def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False, offload=False, tiny=None):
     env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather,
                SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0", SD_TEST_POISON="1" if poison else "0",
                SD_TEST_OFFLOAD="1" if offload else "0")
+    if tiny is not None:
+        env["SD_TEST_TINY"] = str(tiny)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
@@ -196,4 +198,16 @@ def test_offloaded_outer_state_two_ranks_bit_exact(gather):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     rc, out = _run(2, 1024, gather=gather, offload=True)
+    assert rc == 0 and "OK" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull", "mc"])
+@pytest.mark.parametrize("n", [0, 1, 7, 1029])
+def test_tiny_fragments_two_ranks_bit_exact(gather, n):
+    """Degenerate sizes through every gather mode on real ranks: an empty
+    fragment (trailer-only payload), 1 and 7 elements (no full 8-element
+    group), and 1029 (a ragged scale block)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, 1024, gather=gather, tiny=n)
     assert rc == 0 and "OK" in out, out[-3000:]
