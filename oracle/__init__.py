@@ -1,5 +1,8 @@
 """ctypes view of the CPU oracle (oracle/sd_oracle.c).
 
+Two builds of the same C source: liboracle.so (single thread, the oracle
+proper) and liboracle_omp.so (OpenMP, selected by set_threads(n > 1)).
+
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
 bench.py's cpu_baseline / --impl reference legs, never by the product
 package paper_2501_18512_b200/.  See sd_oracle.h for the parity status of
@@ -28,46 +31,75 @@ class OrEvent(ctypes.Structure):
     _fields_ = [("t", ctypes.c_int64), ("kind", ctypes.c_int32), ("p", ctypes.c_int32), ("send_step", ctypes.c_int64)]
 
 
-_lib = None
+_libs = {}
+_active = "liboracle.so"
+_threads = 1
+
+
+def _load(name):
+    return _load_path(os.path.join(_HERE, name))
+
+
+def _load_path(path):
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
+    P, I64, I32, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+    C = ctypes.POINTER(OrConfig)
+    sig = {
+        "or_num_fragments": ([C], I32),
+        "or_fragment_blocks": ([C, I32, P], I32),
+        "or_offset": ([C, I32], I32),
+        "or_calendar": ([C, P, I64], I64),
+        "or_block_scale": ([P, I64], F),
+        "or_e3m0_code": ([F, F], ctypes.c_uint8),
+        "or_e3m0_decode": ([ctypes.c_uint8, F], F),
+        "or_num_scale_blocks": ([I64, I32], I64),
+        "or_payload_bytes": ([I64, I32], ctypes.c_size_t),
+        "or_scales_offset": ([I64], ctypes.c_size_t),
+        "or_quantize": ([P, P, I64, I32, P], ctypes.c_int),
+        "or_payload_poisoned": ([P, I64, I32, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
+        "or_decode_mean": ([P, I32, I64, I32, P], None),
+        "or_nesterov": ([P, P, P, I64, F, F], None),
+        "or_merge": ([P, P, I64, F], None),
+        "or_outer_state_init": ([P, P, P, I64], None),
+        "or_apply": ([P, I32, I64, I32, F, F, F, P, P, P], ctypes.c_int),
+        "or_round": ([I32, I64, I32, F, F, F, P, P, P, P, P], ctypes.c_int),
+        "or_toy_run": ([C, I32, I64, ctypes.c_uint64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
+        "or_adamw": ([P, P, P, P, I64, I64, F, F, F, F, F], None),
+        "or_toy_run_taus": ([C, I32, I64, ctypes.c_uint64, P, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
+    }
+    for fname, (args, res) in sig.items():
+        fn = getattr(L, fname)
+        fn.argtypes = args
+        fn.restype = res
+    return L
 
 
 def lib():
-    global _lib
-    if _lib is None:
-        path = os.path.join(_HERE, "liboracle.so")
-        if not os.path.exists(path):
-            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
-        L = ctypes.CDLL(path)
-        P, I64, I32, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
-        C = ctypes.POINTER(OrConfig)
-        sig = {
-            "or_num_fragments": ([C], I32),
-            "or_fragment_blocks": ([C, I32, P], I32),
-            "or_offset": ([C, I32], I32),
-            "or_calendar": ([C, P, I64], I64),
-            "or_block_scale": ([P, I64], F),
-            "or_e3m0_code": ([F, F], ctypes.c_uint8),
-            "or_e3m0_decode": ([ctypes.c_uint8, F], F),
-            "or_num_scale_blocks": ([I64, I32], I64),
-            "or_payload_bytes": ([I64, I32], ctypes.c_size_t),
-            "or_scales_offset": ([I64], ctypes.c_size_t),
-            "or_quantize": ([P, P, I64, I32, P], ctypes.c_int),
-            "or_payload_poisoned": ([P, I64, I32, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
-            "or_decode_mean": ([P, I32, I64, I32, P], None),
-            "or_nesterov": ([P, P, P, I64, F, F], None),
-            "or_merge": ([P, P, I64, F], None),
-            "or_apply": ([P, I32, I64, I32, F, F, F, P, P, P], ctypes.c_int),
-            "or_round": ([I32, I64, I32, F, F, F, P, P, P, P, P], ctypes.c_int),
-            "or_toy_run": ([C, I32, I64, ctypes.c_uint64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
-            "or_adamw": ([P, P, P, P, I64, I64, F, F, F, F, F], None),
-            "or_toy_run_taus": ([C, I32, I64, ctypes.c_uint64, P, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
-        }
-        for name, (args, res) in sig.items():
-            fn = getattr(L, name)
-            fn.argtypes = args
-            fn.restype = res
-        _lib = L
-    return _lib
+    if _active not in _libs:
+        _libs[_active] = _load(_active)
+    return _libs[_active]
+
+
+def set_threads(n: int) -> int:
+    """n == 1: the single-threaded build (liboracle.so, the oracle proper);
+    n > 1: the same source built with OpenMP (liboracle_omp.so) on n threads.
+    Both produce bit-identical results (tests/test_oracle_omp.py).  Returns
+    the previous thread count."""
+    global _active, _threads
+    prev = _threads
+    if n <= 1:
+        _active, _threads = "liboracle.so", 1
+    else:
+        _active, _threads = "liboracle_omp.so", int(n)
+        lib()
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(ctypes.c_int(int(n)))
+    return prev
+
+
+def threads() -> int:
+    return _threads
 
 
 def _p(a: np.ndarray):
@@ -157,6 +189,15 @@ def nesterov(A, v, g, lr=0.4, mu=0.9):
 
 def merge(theta, A, alpha=0.5):
     lib().or_merge(_p(theta), _p(A), theta.size, alpha)
+
+
+def outer_state_init(theta):
+    """-> (A, v): A_p <- theta_init (bit copy), v_p <- 0."""
+    theta = np.ascontiguousarray(theta, dtype=np.float32)
+    A = np.empty_like(theta)
+    v = np.empty_like(theta)
+    lib().or_outer_state_init(_p(theta), _p(A), _p(v), theta.size)
+    return A, v
 
 
 def apply(gather, M, n, B, A, v, theta, lr=0.4, mu=0.9, alpha=0.5) -> int:

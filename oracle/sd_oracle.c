@@ -4,7 +4,15 @@
  * "S:n" = SPEC.md line n; readings AMB-k are listed in DESIGN.md §2.
  *
  * Build: gcc -std=c99 -O2 -fno-fast-math -ffp-contract=off -shared -fPIC
- *        sd_oracle.c ../synth/synth_cpu.c -lm
+ *        sd_oracle.c ../synth/synth_cpu.c -lm                 -> liboracle.so (1 thread)
+ * and the same source with -fopenmp                           -> liboracle_omp.so
+ * The `omp` pragmas below only split loops whose iterations are independent
+ * (one element, one byte of codes, one scale block); every float operation,
+ * and the ascending-m fold of each element, is the same in both builds, so
+ * the N-thread oracle equals the 1-thread oracle bit for bit (SPEC.md:437,
+ * :614 "determinism under parallelism"; pinned in tests/test_oracle_omp.py).
+ * A max over |Delta| is exact and order-free; the first non-finite index is
+ * a min over indices.
  */
 #include "sd_oracle.h"
 
@@ -82,6 +90,7 @@ int64_t or_calendar(const or_config* c, or_event* out, int64_t cap) {
 /* scale = max |d| over the block (AMB-7); -0 counts as 0. */
 float or_block_scale(const float* d, int64_t len) {
   float s = 0.0f;
+#pragma omp parallel for reduction(max : s) if (len >= (1 << 16))
   for (int64_t i = 0; i < len; ++i) {
     float a = fabsf(d[i]);
     if (a > s) s = a;
@@ -153,18 +162,25 @@ int or_quantize(const float* theta, const float* anchor, int64_t n, int32_t B, u
   uint64_t first_bad = UINT64_MAX;
   memset(payload, 0, bytes);
 
+#pragma omp parallel for reduction(min : first_bad)
   for (int64_t i = 0; i < n; ++i) {
     delta[i] = anchor[i] - theta[i];
-    if (!isfinite(delta[i]) && first_bad == UINT64_MAX) first_bad = (uint64_t)i;
+    if (!isfinite(delta[i]) && (uint64_t)i < first_bad) first_bad = (uint64_t)i;
   }
+  /* B is even (a power of two >= 256) or the block is the whole fragment,
+   * so no byte of codes straddles two blocks */
+#pragma omp parallel for if (nb > 1)
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t lo = b * blen;
     const int64_t len = (lo + blen <= n) ? blen : n - lo;
     const float s = or_block_scale(delta + lo, len);
     memcpy(payload + soff + 4 * (size_t)b, &s, 4);
-    for (int64_t i = lo; i < lo + len; ++i) {
-      const uint8_t c = or_e3m0_code(delta[i], s);
-      payload[i / 2] |= (uint8_t)((i % 2 == 0) ? c : (c << 4));
+    /* byte k = code(2k) | code(2k+1) << 4; an odd tail leaves 0 in the high nibble */
+#pragma omp parallel for if (nb == 1 && len >= (1 << 16))
+    for (int64_t k = lo / 2; k < (lo + len + 1) / 2; ++k) {
+      const uint8_t c0 = or_e3m0_code(delta[2 * k], s);
+      const uint8_t c1 = (2 * k + 1 < lo + len) ? or_e3m0_code(delta[2 * k + 1], s) : 0;
+      payload[k] = (uint8_t)(c0 | (c1 << 4));
     }
   }
   {
@@ -203,6 +219,7 @@ void or_decode_mean(const uint8_t* gather, int32_t M, int64_t n, int32_t B, floa
   const size_t pb = or_payload_bytes(n, B);
   const size_t soff = or_scales_offset(n);
   const int64_t blen = B == 0 ? n : B;
+#pragma omp parallel for
   for (int64_t i = 0; i < n; ++i) {
     float S = 0.0f;
     for (int32_t m = 0; m < M; ++m) {
@@ -222,16 +239,27 @@ void or_decode_mean(const uint8_t* gather, int32_t M, int64_t n, int32_t B, floa
  * "momentum-then-lookahead" form of S:184 (AMB-13):
  *   v <- mu*v + g ;  A <- A - lr*(g + mu*v)   (v already updated) */
 void or_nesterov(float* A, float* v, const float* g, int64_t n, float lr, float mu) {
+#pragma omp parallel for
   for (int64_t i = 0; i < n; ++i) {
     v[i] = mu * v[i] + g[i];
     A[i] = A[i] - lr * (g[i] + mu * v[i]);
   }
 }
 
+/* Outer-state store init ("outer global
+ * parameters" + "outer Nesterov state"): the anchor starts as
+ * the initial parameters, A_p <- theta_init,p (bit copy, AMB-2), and the
+ * outer momentum at zero, v_p <- 0. */
+void or_outer_state_init(const float* theta, float* A, float* v, int64_t n) {
+  memcpy(A, theta, sizeof(float) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) v[i] = 0.0f;
+}
+
 /* alpha-merge (Alg. 2 L13): theta <- alpha*theta + (1-alpha)*A,
  * with beta = 1 - alpha rounded once (AMB-14). */
 void or_merge(float* theta, const float* A, int64_t n, float alpha) {
   const float beta = 1.0f - alpha;
+#pragma omp parallel for
   for (int64_t i = 0; i < n; ++i) theta[i] = alpha * theta[i] + beta * A[i];
 }
 
@@ -432,6 +460,7 @@ void or_adamw(float* theta, const float* g, float* m, float* v, int64_t n, int64
   const float decay = 1.0f - lr * wd;
   const float step = lr / bc1;
   const float sbc2 = sqrtf(bc2);
+#pragma omp parallel for
   for (int64_t i = 0; i < n; ++i) {
     m[i] = b1 * m[i] + c1 * g[i];
     v[i] = b2 * v[i] + c2 * (g[i] * g[i]);

@@ -6,7 +6,8 @@
  * does; the two share no code, header, table or helper.  The one shared
  * module is synth/ (seeded inputs, no method arithmetic).
  *
- * Plain, single-threaded C99 that follows PAPER.md Alg. 2 (lines 103-134)
+ * Plain C99 (liboracle.so: single-threaded; liboracle_omp.so: the same
+ * source built with -fopenmp, bit-identical results) that follows PAPER.md Alg. 2 (lines 103-134)
  * step by step in the paper's order, with SPEC.md's codec and optimizer
  * definitions, under the readings listed in DESIGN.md §2.  Built with
  * -O2 -fno-fast-math -ffp-contract=off: every float operation below rounds
@@ -61,6 +62,7 @@ int or_payload_poisoned(const uint8_t* payload, int64_t n, int32_t B, uint64_t* 
 void or_decode_mean(const uint8_t* gather, int32_t M, int64_t n, int32_t B, float* g);
 void or_nesterov(float* A, float* v, const float* g, int64_t n, float lr, float mu);
 void or_merge(float* theta, const float* A, int64_t n, float alpha);
+void or_outer_state_init(const float* theta, float* A, float* v, int64_t n);
 int or_apply(const uint8_t* gather, int32_t M, int64_t n, int32_t B, float lr, float mu,
              float alpha, float* A, float* v, float* theta);
 int or_round(int32_t M, int64_t n, int32_t B, float lr, float mu, float alpha,

@@ -695,8 +695,12 @@ def test_many_rounds_wide_dynamic_range():
         torch.cuda.synchronize()
         if st != 0:  # a non-finite Delta (huge scale overflow) poisons the round on both sides
             assert all(s[0] == sd.SD_ERR_NONFINITE for s in rep.check_all())
-            A_o = A_d[0].cpu().numpy()
-            v_o = v_d[0].cpu().numpy()
+            # or_round leaves A, v (and theta) untouched on poison; so must every replica
+            # (rank-consistent skip, DESIGN.md §1 errors; PAPER.md:141 / SPEC.md:232)
+            for m in range(M):
+                assert_same(A_d[m], A_o, f"round {r} anchor (poisoned round)")
+                assert_same(v_d[m], v_o, f"round {r} momentum (poisoned round)")
+                assert_same(th_d[m], mo[m], f"round {r} theta (poisoned round)")
             continue
         assert np.array_equal(rep.gather.cpu().numpy(), g_o), f"round {r}: payload bytes differ"
         for m in range(M):
@@ -704,3 +708,26 @@ def test_many_rounds_wide_dynamic_range():
             assert_same(v_d[m], v_o, f"round {r} momentum")
             assert_same(th_d[m], mo[m], f"round {r} theta")
     rep.close()
+
+
+@pytest.mark.parametrize("n", [1, 7, 1024, 300001])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_outer_state_init_matches_oracle(n, inplace):
+    """sd_outer_state_init: A = theta
+    bit for bit (including -0 and NaN payloads), v = +0; the caller's
+    garbage in A and v is overwritten; A may alias theta."""
+    rng = np.random.default_rng(n)
+    raw = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    raw[: min(n, 3)] = [0x80000000, 0x7fc00001, 0x00000001][: min(n, 3)]
+    theta = raw.view(np.float32)
+    A_o, v_o = oracle.outer_state_init(theta)
+    cfg = cfg_for(1024)
+    ctx = sd.SdContext(cfg, 0, 1, None, 0)
+    th = to_dev(theta)
+    A = th if inplace else to_dev(rng.standard_normal(n).astype(np.float32))
+    v = to_dev(np.full(n, np.nan, np.float32))
+    ctx.sd_outer_state_init(th, A, v, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(A), bits(A_o)) and np.array_equal(bits(v), bits(v_o))
+    assert np.array_equal(bits(th), raw)
+    ctx.sd_finalize()

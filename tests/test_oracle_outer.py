@@ -345,3 +345,136 @@ def test_apply_single_replica_fedavg_and_poison(M):
     Aw, v, th = A.copy(), np.zeros(n, np.float32), theta.copy()
     assert oracle.apply(gather, M, n, B, Aw, v, th) != 0
     assert np.array_equal(bits(Aw), bits(A)) and not v.any() and np.array_equal(bits(th), bits(theta))
+
+
+# ------------------------------------------- scale addressing: per slot, per block
+# Every pin above draws its outer gradients with `on_grid`, which puts the
+# same scale 2^-8 in every block of every replica: a decoder reading slot 0's
+# scale (or block 0's) for all (m, b) would still pass them.  The pins below
+# give every (slot m, block b) its own power-of-two scale
+#     s_{m,b} = 2^-(8 + m + 3b)
+# and decode with exact rationals, independently of or_quantize:
+#     q = LUT[c] * s,  LUT[e] = 2^(e-7), LUT[8|e] = -2^(e-7), LUT[0] = LUT[8] = +0
+#     (SPEC.md:245, :264), summed over m and divided by M (
+#     SPEC.md:385).
+# With M <= 8 and b <= 3 every partial sum spans < 24 bits, so the fp32 fold is
+# exact and must equal the rational mean bit for bit.
+from fractions import Fraction  # noqa: E402
+
+
+def _scale(m, b):
+    return 2.0 ** -(8 + m + 3 * b)
+
+
+def _lut(c):
+    e = c & 7
+    if e == 0:
+        return Fraction(0)
+    v = Fraction(2) ** (e - 7)
+    return -v if c & 8 else v
+
+
+def _hand_payload(codes, scales, n, B):
+    """Payload bytes built from the layout definition (S:272 nibble order,
+    DESIGN.md §5 layout), not by or_quantize."""
+    pay = np.zeros(oracle.payload_bytes(n, B), np.uint8)
+    c = np.zeros(2 * ((n + 1) // 2), np.uint8)
+    c[:n] = codes
+    pay[:(n + 1) // 2] = c[0::2] | (c[1::2] << 4)
+    so = oracle.scales_offset(n)
+    nb = len(scales)
+    pay[so:so + 4 * nb] = np.asarray(scales, np.float32).view(np.uint8)
+    to = so + -(-4 * nb // 16) * 16
+    pay[to:to + 4] = np.frombuffer(np.uint32(0x31304453).tobytes(), np.uint8)
+    pay[to + 4:to + 8] = np.frombuffer(np.uint32(nb).tobytes(), np.uint8)
+    pay[to + 8:to + 16] = 0xFF
+    return pay
+
+
+def _rational_mean(codes, n, B, M):
+    blen = B if B else n
+    out = []
+    for i in range(n):
+        b = i // blen
+        S = sum(_lut(int(codes[m][i])) * Fraction(_scale(m, b)) for m in range(M))
+        out.append(S / M)
+    return out
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("B,n", [(256, 4 * 256 - 37), (256, 3 * 256), (0, 700)])
+def test_decode_mean_distinct_scale_per_slot_and_block(M, B, n):
+    rng = np.random.default_rng(7000 + 10 * M + B)
+    nb = oracle.num_scale_blocks(n, B)
+    codes = [rng.integers(0, 16, n).astype(np.uint8) for _ in range(M)]
+    gather = np.concatenate([_hand_payload(codes[m], [_scale(m, b) for b in range(nb)], n, B) for m in range(M)])
+    g = oracle.decode_mean(gather, M, n, B)
+    ref = _rational_mean(codes, n, B, M)
+    if M == 3:  # S/3 rounds: compare with the correctly rounded quotient of the exact (fp32) sum
+        ref = [float(np.float32(float(r * 3)) / np.float32(3)) for r in ref]
+        assert np.array_equal(g.astype(np.float64), np.array(ref))
+    else:
+        assert all(Fraction(float(x)) == r for x, r in zip(g, ref))
+    assert g.any()
+
+
+@pytest.mark.parametrize("M", [1, 2, 4])
+def test_round_and_apply_distinct_scale_per_slot_and_block(M):
+    """or_round (quantize + mean + Nesterov + merge) and or_apply on inputs
+    whose outer gradients have scale s_{m,b} in block b of replica m:
+    with lr = 1, mu = 0, alpha = 0 (FedAvg) the new anchor is
+    A - (1/M) sum_m Delta_m exactly, v = the mean, theta = A'."""
+    rng = np.random.default_rng(800 + M)
+    B, n = 256, 3 * 256 - 11
+    nb = oracle.num_scale_blocks(n, B)
+    # A on a 2^-25 grid with |A| < 2^-2; Delta_{m,i} in {0, +-s_{m,b} 2^-j}:
+    # theta = A - Delta and A - mean are exact in fp32 (<= 24 significant bits)
+    A = (rng.integers(-(2 ** 23) + 1, 2 ** 23, n) * 2.0 ** -25).astype(np.float32)
+    D = []
+    for m in range(M):
+        d = np.zeros(n)
+        for b in range(nb):
+            lo, hi = b * B, min(n, (b + 1) * B)
+            j = rng.integers(-1, 7, hi - lo)
+            v = np.where(j < 0, 0.0, _scale(m, b) * 2.0 ** -np.maximum(j, 0)) * rng.choice([-1.0, 1.0], hi - lo)
+            v[0] = -_scale(m, b) if b % 2 else _scale(m, b)  # the block's max |Delta| is exactly s_{m,b}
+            d[lo:hi] = v
+        D.append(d.astype(np.float32))
+    thetas = [(A - d).astype(np.float32) for d in D]
+    for th, d in zip(thetas, D):
+        assert np.array_equal((A - th).astype(np.float32), d)
+    mean = [sum(Fraction(float(D[m][i])) for m in range(M)) / M for i in range(n)]
+    want_A = [Fraction(float(a)) - g for a, g in zip(A, mean)]
+
+    # scales in the payloads are the distinct s_{m,b}
+    pays = [oracle.quantize(th, A, B)[0] for th in thetas]
+    so = oracle.scales_offset(n)
+    for m in range(M):
+        assert pays[m][so:so + 4 * nb].view(np.float32).tolist() == [_scale(m, b) for b in range(nb)]
+
+    merges = [t.copy() for t in thetas]
+    Aw, v = A.copy(), np.zeros(n, np.float32)
+    st, _ = oracle.round_(thetas, merges, Aw, v, B=B, lr=1.0, mu=0.0, alpha=0.0)
+    assert st == 0
+    assert all(Fraction(float(x)) == w for x, w in zip(Aw, want_A))
+    assert all(Fraction(float(x)) == g for x, g in zip(v, mean))
+    for mth in merges:
+        assert np.array_equal(bits(mth), bits(Aw))
+
+    Aw2, v2, th2 = A.copy(), np.zeros(n, np.float32), thetas[0].copy()
+    assert oracle.apply(np.concatenate(pays), M, n, B, Aw2, v2, th2, lr=1.0, mu=0.0, alpha=0.0) == 0
+    assert np.array_equal(bits(Aw2), bits(Aw)) and np.array_equal(bits(v2), bits(v))
+    assert np.array_equal(bits(th2), bits(Aw))
+
+
+def test_outer_state_init_is_bit_copy_and_zero():
+    """A_p <- theta_init, v_p <- 0:
+    the anchor is the parameters' bit pattern (including -0 and NaN
+    payloads), the momentum is +0 everywhere."""
+    rng = np.random.default_rng(3)
+    raw = rng.integers(0, 2 ** 32, 4099, dtype=np.uint64).astype(np.uint32)
+    raw[:4] = [0x80000000, 0x7fc00001, 0xff800000, 0x00000001]
+    theta = raw.view(np.float32)
+    A, v = oracle.outer_state_init(theta)
+    assert np.array_equal(A.view(np.uint32), raw)
+    assert not v.view(np.uint32).any()
