@@ -36,11 +36,10 @@
  *  - One sd_ctx per replica (= per GPU process), used from one host thread
  *    in program order.  The schedule functions are pure and thread-safe.
  *  - Layout: a fragment is one contiguous fp32 slab of n elements (AMB-18).
- *  - Environment (read once per process; measurement switches, results are
- *    bit-identical either way): SD_QUANTIZE_TMA=1 / SD_APPLY_TMA=1 select the
- *    bulk-copy (TMA) staged quantize / apply kernels, measured slower than the
- *    default direct-load kernels; SD_BLOCKS_PER_SM=k caps the
- *    grids at k CTAs per SM.
+ *  - Environment (read once per process): SD_BLOCKS_PER_SM=k caps the grids
+ *    at k CTAs per SM (measurement switch, results bit-identical);
+ *    SD_WAIT_TIMEOUT_MS bounds the fused gathers' block-receive (below);
+ *    SD_LOG_INIT=1 prints one line per communicator set up (stderr).
  */
 #ifndef SD_H_
 #define SD_H_
@@ -176,29 +175,33 @@ sd_status sd_gather_free(sd_ctx* ctx, void* gather_buf);
  *                         block-receive is an acquire-wait on the peers'
  *                         flags.  Buffers hold two rounds (alternating by
  *                         round id), so no rendezvous is needed.
- *  SD_GATHER_MULTICAST    zero-SM, one HBM read per payload: the quantize
- *                         writes a staging slot; the sync has the copy
- *                         engine write it once through the gather window's
- *                         NVLS multicast alias (NCCL device API, LSA-team
- *                         multimem), NVSwitch delivers it into every rank's
- *                         slot, then a one-thread kernel release-signals the
- *                         round flag as in PUSH.  Falls back to COPY_ENGINE
- *                         where the system has no multicast.
- * In PUSH, PULL and MULTICAST modes the block-receive waits at most 30 s
- * (SD_WAIT_TIMEOUT_MS overrides) for each peer's round flag; on a timeout
- * the round is skipped on this rank (A, v, theta untouched) and sd_check
- * reports SD_ERR_STATE.
+ * SD_GATHER_PULL is the same protocol with the transfer fused into the merge
+ * instead (the apply reads the peers' slots from their buffers over NVLink).
+ * In both, the round signal is fused into the end of the kernel that
+ * finishes the payload (its last CTA release-stores {round id, first
+ * non-finite index} into each peer's flag entry); the block-receive is one
+ * single-CTA kernel per round that acquire-waits on the local flag entries
+ * and leaves its verdict for the apply's CTAs.
+ * The fused modes need every rank in this rank's NVLink (LSA) team and
+ * M <= 32; otherwise (or without a communicator) the copy engines carry the
+ * gather.
+ * Block-receive timeout (PUSH, PULL): none by default -- the wait kernel
+ * waits for every peer's flag.  SD_WAIT_TIMEOUT_MS=<ms> bounds it; on a timeout the round is skipped on this rank (A, v,
+ * theta untouched), this rank tells its peers (a peer that has not passed its
+ * own wait for the round skips it too), and the context becomes unusable:
+ * sd_check and every later device call return SD_ERR_STATE, because the
+ * replicas' outer state may no longer be identical -- re-initialize every
+ * replica from a common state.
  * With caller-owned buffers or without a communicator the mode is ignored.
- * In PUSH, PULL and MULTICAST modes a gather buffer must serve a single
- * fragment (its round ids count that fragment's sends). */
+ * In PUSH and PULL modes a gather buffer must serve a single fragment (its
+ * round ids count that fragment's sends). */
 #define SD_GATHER_COPY_ENGINE 0
 #define SD_GATHER_PUSH 1
 #define SD_GATHER_AUTO 2 /* default: COPY_ENGINE when tau >= 1 (hidden behind later work); with tau == 0
                             (nothing to overlap with) PULL for M in {4, 8}, else PUSH -- measured on B200 */
 #define SD_GATHER_PULL 3 /* fused into the apply: the quantize writes locally and signals; the merge
                             kernel reads the peers' payloads from their buffers over NVLink (no HBM
-                            staging of the M payloads); M in {2, 4, 8}, else COPY_ENGINE */
-#define SD_GATHER_MULTICAST 4
+                            staging of the M payloads) */
 sd_status sd_set_gather_mode(sd_ctx* ctx, int32_t mode);
 
 /* Address of the M payloads of fragment p's most recent round inside
@@ -222,13 +225,22 @@ sd_status sd_outer_state_init(sd_ctx* ctx, const float* theta, float* anchor, fl
  *    copies on the copy stream.  p must not be in flight.
  *  sd_state_sync: `stream` waits for every copy issued so far (e.g. before
  *    reading the host store or reusing the host buffers).
- * Copies are FIFO on one copy stream, so a prefetch into a staging buffer
- * never overtakes the writeback of its previous contents. */
+ * Prefetches run on one copy stream (host -> device), writebacks on another
+ * (device -> host), so the two directions overlap (PCIe is full duplex); a
+ * prefetch into a staging buffer waits for the last writeback out of that
+ * buffer, and a writeback waits for the prefetches issued before it (so it
+ * never overwrites host data a prefetch is still reading). */
 sd_status sd_state_prefetch(sd_ctx* ctx, int32_t p, const float* anchor_host, const float* momentum_host,
                             float* anchor, float* momentum, int64_t n, sd_stream stream);
 sd_status sd_state_writeback(sd_ctx* ctx, int32_t p, const float* anchor, const float* momentum,
                              float* anchor_host, float* momentum_host, int64_t n, sd_stream stream);
 sd_status sd_state_sync(sd_ctx* ctx, sd_stream stream);
+
+/* The ctx's communication stream (highest priority; the copy-engine
+ * all-gather of sd_fragment_sync runs on it), for tracing and timelines:
+ * an event recorded on it after sd_fragment_sync completes with the gather.
+ * Owned by the ctx; do not enqueue work on it. */
+sd_status sd_comm_stream(sd_ctx* ctx, sd_stream* out);
 
 /* InnerOpt = AdamW (NEXT-1; Alg. 2 L5; Adam as InnerOpt, P:77;
  * SPEC.md:171-179 adamw_step with decoupled weight decay). */
@@ -295,8 +307,10 @@ sd_status sd_inner_adamw_merge(sd_ctx* ctx, int32_t p, int64_t t, int64_t k, flo
                                int64_t n, const sd_adamw* hp, sd_stream stream);
 
 /* Synchronizes the device and reports deferred errors: CUDA errors, NCCL
- * async errors, and a skipped (poisoned) round — then SD_ERR_NONFINITE and
- * *first_bad_index (if non-NULL) = index of the first non-finite Delta. */
+ * async errors, and a skipped round -- SD_ERR_NONFINITE with
+ * *first_bad_index (if non-NULL) = index of the first non-finite Delta for
+ * a poisoned round; SD_ERR_STATE for a malformed payload, or (sticky) for a
+ * block-receive timeout (SD_WAIT_TIMEOUT_MS). */
 sd_status sd_check(sd_ctx* ctx, int64_t* first_bad_index);
 
 /* Message of the last failing call on ctx (thread-local one if ctx == NULL). */

@@ -3,6 +3,7 @@
 // in-flight table) and the C ABI of include/sd.h.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>  // ncclTeamLsa (host side of the NCCL 2.28 device API)
 
 #include <atomic>
 #include <cmath>
@@ -125,10 +126,9 @@ struct Inflight {
   const void* gather = nullptr;
   bool push = false;      // two-round symmetric buffer with round flags (PUSH or PULL mode)
   bool pull = false;      // PULL: the apply reads the peers' slots over NVLink
-  bool mc = false;        // MULTICAST: the sync copies the staged payload through the multicast alias
-  bool waited = false;    // push mode: the block-receive wait kernel was issued
-  size_t half_off = 0;    // push mode: byte offset of this round's half
-  uint64_t seq = 0;       // push mode: round id published in the peers' flags
+  bool waited = false;    // bounded wait: k_round_wait was issued for this round
+  size_t half_off = 0;    // push / pull: byte offset of this round's half
+  uint64_t seq = 0;       // push / pull: round id published in the peers' flags
 };
 
 }  // namespace
@@ -138,12 +138,15 @@ struct GatherBuf {
   size_t bytes = 0;
   ncclWindow_t win = nullptr;
   bool nccl = false;
-  bool push = false;   // two-round layout: halves (round parity) of M payloads + M round flags (PUSH/PULL)
+  bool push = false;   // two-round layout: halves (round parity) of M payloads + round flags (PUSH/PULL)
   bool pull = false;   // PULL mode: peers' payloads stay in the peers' buffers, read by the apply
-  bool mc = false;     // MULTICAST mode: staging slot at 2*half, copied through the multicast alias
-  uint8_t* mc_base = nullptr;  // multicast address of byte 0 of the buffer
   size_t half = 0;     // bytes per half
   size_t pb = 0;       // payload bytes
+  // layout of a half (push / pull): [M payloads][M flag entries {round id, first_bad}]
+  //                                 [verdict {first_bad, code}][last-CTA counter]
+  size_t flags_rel(int M) const { return (size_t)M * pb; }
+  size_t verdict_rel(int M) const { return flags_rel(M) + 16 * (size_t)M; }
+  size_t counter_rel(int M) const { return verdict_rel(M) + 16; }
 };
 
 struct sd_ctx {
@@ -153,16 +156,24 @@ struct sd_ctx {
   std::vector<uint64_t> round_seq;  // push mode: sends of each fragment so far (round id, same on every rank)
   int32_t rank = 0, M = 1, device = 0, P = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
-  sdk::McState* mc = nullptr;  // NCCL device communicator with the multimem handle (MULTICAST mode)
-  int mc_state = 0;            // 0 not tried, 1 available, -1 unavailable
+  bool lsa_all = false;        // every rank is in this rank's NVLink (LSA) team: PUSH / PULL possible
+  bool dead = false;           // a bounded block-receive timed out: every later device call fails (sticky)
   cudaStream_t comm_stream = nullptr;
-  cudaStream_t copy_stream = nullptr;               // outer-state offload (NEXT-3)
+  cudaStream_t copy_stream = nullptr;               // outer-state offload (NEXT-3): host -> device
+  cudaStream_t wb_stream = nullptr;                 // outer-state offload: device -> host (full duplex)
   std::vector<cudaEvent_t> ready, done;
   std::vector<cudaEvent_t> staged;                   // prefetch of fragment p landed
   std::vector<char> prefetch_pending;                // quantize must wait on staged[p]
   cudaEvent_t copy_gate = nullptr;
+  // last writeback out of each device staging buffer (by anchor address): a
+  // prefetch into that buffer waits for it; other copies run concurrently
+  struct Drain {
+    const void* staging;
+    cudaEvent_t ev;
+  };
+  std::vector<Drain> drains;
   std::vector<Inflight> fl;
-  unsigned long long* status_host = nullptr;  // {first_bad, flags}: pinned, mapped
+  unsigned long long* status_host = nullptr;  // {first_bad, code, dead}: pinned, mapped
   unsigned long long* status_dev = nullptr;
   char err[512] = "";
 };
@@ -345,6 +356,8 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreateWithPriority"));
   e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreate(copy)"));
+  e = cudaStreamCreateWithFlags(&c->wb_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaStreamCreate(writeback)"));
   e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaEventCreate(copy_gate)"));
   c->staged.assign((size_t)c->P, nullptr);
@@ -360,10 +373,11 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming);
     if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaEventCreate"));
   }
-  e = cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), 2 * sizeof(unsigned long long), cudaHostAllocMapped);
+  e = cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), 3 * sizeof(unsigned long long), cudaHostAllocMapped);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaHostAlloc(status)"));
   c->status_host[0] = ~0ull;
   c->status_host[1] = 0;
+  c->status_host[2] = 0;
   e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->status_dev), c->status_host, 0);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaHostGetDevicePointer"));
   if (id && M > 1) {
@@ -378,6 +392,12 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
       fail(g_err, SD_ERR_NCCL, "ncclCommInitRank(M=%d, rank=%d): %s", M, rank, ncclGetErrorString(r));
       return bail(SD_ERR_NCCL);
     }
+    // the fused gathers address every peer through NVLink (LSA) pointers indexed by rank
+    const ncclTeam_t lsa = ncclTeamLsa(c->comm);
+    c->lsa_all = lsa.nRanks == M && lsa.rank == rank && M <= 32;
+    if (getenv("SD_LOG_INIT"))
+      fprintf(stderr, "[libsd] rank %d/%d: NCCL communicator up on device %d (LSA team %d ranks, fused gathers %s)\n",
+              rank, M, device, lsa.nRanks, c->lsa_all ? "available" : "off");
   }
   *out = c;
   return SD_OK;
@@ -405,24 +425,19 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
   b.pb = payload_of(&c->cfg, n).bytes;
   // AUTO, from B200 measurements: with tau >= 1 the copy-engine
   // gather hides behind the next kernels; with tau = 0 it is on the critical
-  // path and a fused variant wins -- the push at M = 2, the pull at M = 4, 8
+  // path and a fused variant wins -- the push at M = 2, the pull at M = 4, 8.
+  // The fused modes need every rank in this rank's NVLink (LSA) team and
+  // M <= 32 (one flag entry and, in pull mode, one slot pointer per peer);
+  // otherwise the copy engines carry the gather.
   int mode = c->gather_mode;
   if (mode == SD_GATHER_AUTO)
     mode = c->cfg.tau > 0 ? SD_GATHER_COPY_ENGINE : ((c->M == 4 || c->M == 8) ? SD_GATHER_PULL : SD_GATHER_PUSH);
-  if (mode == SD_GATHER_PULL && !(c->M == 2 || c->M == 4 || c->M == 8)) mode = SD_GATHER_COPY_ENGINE;
-  if (mode == SD_GATHER_MULTICAST && c->comm && c->mc_state == 0) {
-    // collective: every rank allocates its gather buffers in the same order and mode
-    const int r = sdk::mc_create(c->comm, &c->mc);
-    if (r < 0) return ctx_fail(c, SD_ERR_NCCL, "ncclDevCommCreate(lsaMultimem) failed");
-    c->mc_state = r == 1 ? 1 : -1;
-  }
-  if (mode == SD_GATHER_MULTICAST && c->mc_state != 1) mode = SD_GATHER_COPY_ENGINE;  // no NVLS here
-  b.push = c->comm && (mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL || mode == SD_GATHER_MULTICAST);
+  if ((mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL) && !c->lsa_all) mode = SD_GATHER_COPY_ENGINE;
+  b.push = c->comm && (mode == SD_GATHER_PUSH || mode == SD_GATHER_PULL);
   b.pull = b.push && mode == SD_GATHER_PULL;
-  b.mc = b.push && mode == SD_GATHER_MULTICAST;
   if (b.push) {
-    b.half = (size_t)align_up((int64_t)(b.pb * (size_t)c->M) + 256, 256);
-    b.bytes = (size_t)align_up((int64_t)(2 * b.half + (b.mc ? b.pb : 0)), 2 << 20);
+    b.half = (size_t)align_up((int64_t)(b.pb * (size_t)c->M + 16 * (size_t)c->M + 64), 256);
+    b.bytes = (size_t)align_up((int64_t)(2 * b.half), 2 << 20);
   } else {
     b.bytes = (size_t)align_up((int64_t)(b.pb * (size_t)c->M), 2 << 20);
   }
@@ -430,7 +445,7 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
     ncclResult_t r = ncclMemAlloc(&b.ptr, b.bytes);
     if (r != ncclSuccess) return ctx_fail(c, SD_ERR_NCCL, "ncclMemAlloc(%zu): %s", b.bytes, ncclGetErrorString(r));
     if (b.push) {
-      // round flags start at 0 (never a round id).  Zeroed BEFORE the
+      // round flags and counters start at 0 (never a round id).  Zeroed BEFORE the
       // collective registration: once any rank returns from it, every rank
       // has finished its memset, so no peer's first push can be overwritten
       cudaError_t e = cudaMemset(b.ptr, 0, b.bytes);
@@ -446,10 +461,6 @@ sd_status sd_gather_alloc(sd_ctx* c, int64_t n, void** out) {
       return ctx_fail(c, SD_ERR_NCCL, "ncclCommWindowRegister(%zu): %s", b.bytes, ncclGetErrorString(r));
     }
     b.nccl = true;
-    if (b.mc && sdk::mc_base(c->mc, b.win, &b.mc_base, c->comm_stream) < 0) {
-      release(c, b);
-      return ctx_fail(c, SD_ERR_CUDA, "multicast address of the gather window: %s", cudaGetErrorString(cudaGetLastError()));
-    }
   } else {
     SD_CUDA(c, cudaMalloc(&b.ptr, b.bytes));
   }
@@ -486,10 +497,8 @@ sd_status sd_gather_payloads(sd_ctx* c, int32_t p, const void* gather_buf, const
 
 sd_status sd_set_gather_mode(sd_ctx* c, int32_t mode) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
-  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO && mode != SD_GATHER_PULL &&
-      mode != SD_GATHER_MULTICAST)
-    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, _PUSH, _PULL, _MULTICAST or _AUTO",
-                    mode);
+  if (mode != SD_GATHER_COPY_ENGINE && mode != SD_GATHER_PUSH && mode != SD_GATHER_AUTO && mode != SD_GATHER_PULL)
+    return ctx_fail(c, SD_ERR_ARG, "gather mode %d is not SD_GATHER_COPY_ENGINE, _PUSH, _PULL or _AUTO", mode);
   for (const Inflight& f : c->fl)
     if (f.state != IDLE) return ctx_fail(c, SD_ERR_STATE, "gather mode changed while a fragment is in flight");
   c->gather_mode = mode;
@@ -523,8 +532,11 @@ sd_status sd_state_prefetch(sd_ctx* c, int32_t p, const float* anchor_host, cons
     return st;
   SD_CUDA(c, cudaSetDevice(c->device));
   // the staging slot is free once `stream`'s prior work (the last user of the slot) is done
+  // and the last writeback out of it has finished
   SD_CUDA(c, cudaEventRecord(c->copy_gate, static_cast<cudaStream_t>(stream)));
   SD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
+  for (const sd_ctx::Drain& d : c->drains)
+    if (d.staging == anchor || d.staging == momentum) SD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, d.ev, 0));
   SD_CUDA(c, cudaMemcpyAsync(anchor, anchor_host, 4 * (size_t)n, cudaMemcpyHostToDevice, c->copy_stream));
   SD_CUDA(c, cudaMemcpyAsync(momentum, momentum_host, 4 * (size_t)n, cudaMemcpyHostToDevice, c->copy_stream));
   SD_CUDA(c, cudaEventRecord(c->staged[p], c->copy_stream));
@@ -545,9 +557,21 @@ sd_status sd_state_writeback(sd_ctx* c, int32_t p, const float* anchor, const fl
     return st;
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaEventRecord(c->copy_gate, static_cast<cudaStream_t>(stream)));  // after the merge
-  SD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
-  SD_CUDA(c, cudaMemcpyAsync(anchor_host, anchor, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->copy_stream));
-  SD_CUDA(c, cudaMemcpyAsync(momentum_host, momentum, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->copy_stream));
+  SD_CUDA(c, cudaStreamWaitEvent(c->wb_stream, c->copy_gate, 0));
+  // a writeback of host buffers that a prefetch is still reading must not overtake it
+  SD_CUDA(c, cudaEventRecord(c->copy_gate, c->copy_stream));
+  SD_CUDA(c, cudaStreamWaitEvent(c->wb_stream, c->copy_gate, 0));
+  SD_CUDA(c, cudaMemcpyAsync(anchor_host, anchor, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->wb_stream));
+  SD_CUDA(c, cudaMemcpyAsync(momentum_host, momentum, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->wb_stream));
+  sd_ctx::Drain* d = nullptr;
+  for (sd_ctx::Drain& x : c->drains)
+    if (x.staging == anchor) d = &x;
+  if (!d) {
+    c->drains.push_back({anchor, nullptr});
+    d = &c->drains.back();
+    SD_CUDA(c, cudaEventCreateWithFlags(&d->ev, cudaEventDisableTiming));
+  }
+  SD_CUDA(c, cudaEventRecord(d->ev, c->wb_stream));
   return SD_OK;
 }
 
@@ -556,6 +580,15 @@ sd_status sd_state_sync(sd_ctx* c, sd_stream stream) {
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaEventRecord(c->copy_gate, c->copy_stream));
   SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->copy_gate, 0));
+  SD_CUDA(c, cudaEventRecord(c->copy_gate, c->wb_stream));
+  SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->copy_gate, 0));
+  return SD_OK;
+}
+
+sd_status sd_comm_stream(sd_ctx* c, sd_stream* out) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (!out) return ctx_fail(c, SD_ERR_ARG, "out pointer is NULL");
+  *out = static_cast<sd_stream>(c->comm_stream);
   return SD_OK;
 }
 
@@ -577,49 +610,59 @@ sd_status sd_outer_state_init(sd_ctx* c, const float* theta, float* anchor, floa
 
 namespace {
 
-// Push mode: where this round's payloads live and the push spec of the quantize.
+// Push / pull modes: where this round's payloads live and the send side of the protocol.
 struct PushRound {
   GatherBuf* buf = nullptr;
   size_t half_off = 0;
   uint64_t seq = 0;
   bool pull = false;
-  bool mc = false;
-  sdk::Push push;
+  sdk::Round round;
 };
 
-sd_status push_round(sd_ctx* c, int32_t p, int64_t t, void* slot_out, const sdk::Payload& pl, PushRound* r) {
+sd_status push_round(sd_ctx* c, int32_t p, void* slot_out, const sdk::Payload& pl, PushRound* r) {
   GatherBuf* b = find_buf(c, slot_out);
   if (!b || !b->push) return SD_OK;
   if (b->pb != pl.bytes) return ctx_fail(c, SD_ERR_ARG, "gather buffer was allocated for payloads of %zu bytes, not %zu", b->pb, pl.bytes);
   if (static_cast<char*>(slot_out) != static_cast<char*>(b->ptr) + (size_t)c->rank * pl.bytes)
     return ctx_fail(c, SD_ERR_ARG, "slot_out must be gather_buf + rank * payload");
-  (void)t;
   r->seq = c->round_seq[p] + 1;  // this send's round id (identical on every rank: same call sequence)
   r->buf = b;
   r->half_off = (size_t)(r->seq & 1) * b->half;
-  if (!b->pull && !b->mc) {  // PUSH: the quantize stores into the peers' buffers
-    r->push.win = b->win;
-    r->push.win_off = r->half_off + (size_t)c->rank * pl.bytes;
-    r->push.rank = c->rank;
-    r->push.M = c->M;
-  }
   r->pull = b->pull;
-  r->mc = b->mc;
+  r->round.win = b->win;
+  r->round.win_off = r->half_off + (size_t)c->rank * pl.bytes;
+  r->round.flags_off = r->half_off + b->flags_rel(c->M);
+  r->round.counter = reinterpret_cast<unsigned int*>(static_cast<char*>(b->ptr) + r->half_off + b->counter_rel(c->M));
+  r->round.seq = r->seq;
+  r->round.rank = c->rank;
+  r->round.M = c->M;
+  r->round.push = !b->pull;
   return SD_OK;
 }
 
-// Checks shared by the two quantizing calls; on success the stream has waited
-// for a pending outer-state prefetch and the trailer's first_bad is reset.
+// The payload's local slot: this round's half in push / pull modes.
 uint8_t* local_slot(sd_ctx* c, void* slot_out, const PushRound& pr, const sdk::Payload& pl) {
   if (!pr.buf) return static_cast<uint8_t*>(slot_out);
-  if (pr.mc) return static_cast<uint8_t*>(pr.buf->ptr) + 2 * pr.buf->half;  // staging slot
   return static_cast<uint8_t*>(pr.buf->ptr) + pr.half_off + (size_t)c->rank * pl.bytes;
+}
+
+// A bounded block-receive timed out earlier (sticky): the replicas' outer
+// state may have diverged, so every later device call is refused.
+sd_status check_alive(sd_ctx* c) {
+  if (!c->dead && c->status_host && *reinterpret_cast<volatile unsigned long long*>(c->status_host + 2) != 0)
+    c->dead = true;
+  if (c->dead)
+    return ctx_fail(c, SD_ERR_STATE,
+                    "a block-receive timed out on this context: the replicas' outer state may differ; "
+                    "re-initialize every replica from a common state (sd_finalize + sd_init)");
+  return SD_OK;
 }
 
 sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor, int64_t n,
                      void* slot_out, cudaStream_t s, sdk::Payload* pl, PushRound* pr) {
   sd_status st;
   if ((st = check_fragment(c, p, t, n))) return st;
+  if ((st = check_alive(c))) return st;
   if ((c->cfg.T == 0 || t <= c->cfg.T) ? !sends_at(&c->cfg, p, t) : true)
     return ctx_fail(c, SD_ERR_SCHEDULE, "fragment %d is not scheduled to send at step %lld (t_p = %d, H = %d)", p,
                     (long long)t, offset_of(&c->cfg, p), c->cfg.H);
@@ -629,7 +672,7 @@ sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const 
   if ((st = check_ptr(c, slot_out, 256, "slot_out"))) return st;
   if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")))) return st;
   *pl = payload_of(&c->cfg, n);
-  if ((st = push_round(c, p, t, slot_out, *pl, pr))) return st;
+  if ((st = push_round(c, p, slot_out, *pl, pr))) return st;
   SD_CUDA(c, cudaSetDevice(c->device));
   if (c->prefetch_pending[p]) {  // offloaded outer state: the anchor must have landed
     SD_CUDA(c, cudaStreamWaitEvent(s, c->staged[p], 0));
@@ -639,29 +682,14 @@ sd_status begin_send(sd_ctx* c, int32_t p, int64_t t, const float* theta, const 
   return SD_OK;
 }
 
-sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, const PushRound& pr,
-                   const sdk::Payload& pl, cudaStream_t s) {
-  if (pr.buf && pr.mc) {  // multicast: the sync copies and signals
-    c->round_seq[p] = pr.seq;
-  } else if (pr.buf) {  // fused all-gather: publish this round to the peers
-    sdk::Push sig = pr.push;  // the signal reaches every peer in both modes
-    sig.win = pr.buf->win;
-    sig.win_off = pr.half_off + (size_t)c->rank * pl.bytes;
-    sig.rank = c->rank;
-    sig.M = c->M;
-    const int k = sdk::launch_push_signal(pl, local_slot(c, slot_out, pr, pl), sig,
-                                          pr.half_off + (size_t)c->M * pl.bytes, pr.seq, s);
-    if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_signal launch");
-    g_launches += (uint64_t)k;
-    c->round_seq[p] = pr.seq;
-  }
+sd_status end_send(sd_ctx* c, int32_t p, int64_t t, int64_t n, void* slot_out, const PushRound& pr) {
+  if (pr.buf) c->round_seq[p] = pr.seq;  // the kernel's last CTA has signalled the peers
   c->fl[p].state = QUANTIZED;
   c->fl[p].send_step = t;
   c->fl[p].n = n;
   c->fl[p].slot = slot_out;
   c->fl[p].push = pr.buf != nullptr;
   c->fl[p].pull = pr.pull;
-  c->fl[p].mc = pr.mc;
   c->fl[p].waited = false;
   c->fl[p].half_off = pr.half_off;
   c->fl[p].seq = pr.seq;
@@ -701,10 +729,10 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
   PushRound pr;
   sd_status st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
-  const int k = sdk::launch_quantize(theta, anchor, pl, local_slot(c, slot_out, pr, pl), pr.push, c->num_sms, s);
+  const int k = sdk::launch_quantize(theta, anchor, pl, local_slot(c, slot_out, pr, pl), pr.round, c->num_sms, s);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
   g_launches += (uint64_t)k;
-  return end_send(c, p, t, n, slot_out, pr, pl, s);
+  return end_send(c, p, t, n, slot_out, pr);
 }
 
 sd_status sd_inner_adamw(sd_ctx* c, int64_t k, float* theta, const float* grad, float* m, float* v, int64_t n,
@@ -741,10 +769,10 @@ sd_status sd_inner_adamw_quantize(sd_ctx* c, int32_t p, int64_t t, int64_t k, fl
   st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
   const int kl = sdk::launch_adamw_quantize(theta, grad, m, v, anchor, pl, local_slot(c, slot_out, pr, pl), h,
-                                            pr.push, c->num_sms, s);
+                                            pr.round, c->num_sms, s);
   if (kl < 0) return cuda_fail(c, cudaGetLastError(), "k_adamw_quantize launch");
   g_launches += (uint64_t)kl;
-  return end_send(c, p, t, n, slot_out, pr, pl, s);
+  return end_send(c, p, t, n, slot_out, pr);
 }
 
 sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, int64_t n, sd_stream stream) {
@@ -763,19 +791,8 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
                     c->rank, pl.bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SD_CUDA(c, cudaSetDevice(c->device));
-  if (f.mc) {  // one copy-engine write through the multicast alias reaches every rank's slot
-    GatherBuf* b = find_buf(c, gather_buf);
-    if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: multicast gather buffer not found", p);
-    SD_CUDA(c, cudaEventRecord(c->ready[p], s));
-    SD_CUDA(c, cudaStreamWaitEvent(c->comm_stream, c->ready[p], 0));
-    SD_CUDA(c, cudaMemcpyAsync(b->mc_base + f.half_off + (size_t)c->rank * pl.bytes, static_cast<uint8_t*>(b->ptr) + 2 * b->half,
-                               pl.bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-    const int k = sdk::launch_flag_signal(b->win, f.half_off + (size_t)c->M * pl.bytes, c->rank, c->M, f.seq,
-                                          c->comm_stream);
-    if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_flag_signal launch");
-    g_launches += (uint64_t)k;
-    SD_CUDA(c, cudaEventRecord(c->done[p], c->comm_stream));
-  } else if (f.push) {  // the payloads were pushed by the quantize: nothing to transfer
+  if ((st = check_alive(c))) return st;
+  if (f.push) {  // push: the quantize stored the payload into the peers; pull: the apply reads it
     SD_CUDA(c, cudaEventRecord(c->done[p], s));
   } else if (c->comm) {
     SD_CUDA(c, cudaEventRecord(c->ready[p], s));
@@ -792,30 +809,44 @@ sd_status sd_fragment_sync(sd_ctx* c, int32_t p, int64_t t, void* gather_buf, in
 }
 
 namespace {
-// Bound of the block-receive spin on the peers' round flags: 30 s, or
-// SD_WAIT_TIMEOUT_MS (read once; tests shorten it to exercise the timeout).
+// Bound of the block-receive wait on the peers' round flags (push / pull
+// modes): SD_WAIT_TIMEOUT_MS (read once per process), 0 or unset = no bound.
 uint64_t wait_timeout_ns() {
-  static uint64_t ns = 0;
-  if (ns == 0) {
+  static int64_t ns = -1;
+  if (ns < 0) {
     const char* e = getenv("SD_WAIT_TIMEOUT_MS");
     const long long ms = e ? atoll(e) : 0;
-    ns = (ms > 0 ? (uint64_t)ms : 30000ull) * 1000000ull;
+    ns = ms > 0 ? (int64_t)ms * 1000000ll : 0;
   }
-  return ns;
+  return (uint64_t)ns;
 }
 
-// push mode block-receive: one wait kernel per round (bounded per peer)
-sd_status issue_push_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
+// The receive side of this round (push / pull modes).
+sdk::RoundRecv round_recv(sd_ctx* c, const Inflight& f, GatherBuf* b) {
+  sdk::RoundRecv rr;
+  const sdk::Payload pl = payload_of(&c->cfg, f.n);
+  uint8_t* half = static_cast<uint8_t*>(b->ptr) + f.half_off;
+  rr.flags = reinterpret_cast<const unsigned long long*>(half + b->flags_rel(c->M));
+  rr.own = half + (size_t)c->rank * pl.bytes;
+  rr.verdict = reinterpret_cast<unsigned long long*>(half + b->verdict_rel(c->M));
+  rr.seq = f.seq;
+  rr.rank = c->rank;
+  rr.pull = f.pull;
+  rr.win = b->win;
+  rr.half_off = f.half_off;
+  rr.flags_off = f.half_off + b->flags_rel(c->M);
+  return rr;
+}
+
+// block-receive of the fused gathers: one k_round_wait per round
+sd_status issue_round_wait(sd_ctx* c, int32_t p, cudaStream_t s) {
   Inflight& f = c->fl[p];
   if (!f.push || f.waited) return SD_OK;
   GatherBuf* b = find_buf(c, f.gather);
-  if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: push-mode gather buffer not found", p);
-  const sdk::Payload pl = payload_of(&c->cfg, f.n);
-  uint8_t* half = static_cast<uint8_t*>(b->ptr) + f.half_off;
-  const int k = sdk::launch_push_wait(reinterpret_cast<const unsigned long long*>(half + (size_t)c->M * pl.bytes),
-                                      half, pl, c->M, c->rank, f.seq, wait_timeout_ns(),
-                                      c->status_dev, s);
-  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_push_wait launch");
+  if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: push/pull-mode gather buffer not found", p);
+  const sdk::RoundRecv rr = round_recv(c, f, b);
+  const int k = sdk::launch_round_wait(rr, payload_of(&c->cfg, f.n), c->M, wait_timeout_ns(), c->status_dev, s);
+  if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_round_wait launch");
   g_launches += (uint64_t)k;
   f.waited = true;
   return SD_OK;
@@ -833,9 +864,10 @@ sd_status sd_fragment_wait(sd_ctx* c, int32_t p, int64_t t, sd_stream stream) {
   if (c->fl[p].state != SYNCED || c->fl[p].send_step != s_step)
     return ctx_fail(c, SD_ERR_STATE, "fragment %d: wait at step %lld needs the sync of step %lld first", p,
                     (long long)t, (long long)s_step);
+  if ((st = check_alive(c))) return st;
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->done[p], 0));
-  return issue_push_wait(c, p, static_cast<cudaStream_t>(stream));
+  return issue_round_wait(c, p, static_cast<cudaStream_t>(stream));
 }
 
 namespace {
@@ -854,6 +886,7 @@ sd_status do_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   if (f.n != n) return ctx_fail(c, SD_ERR_ARG, "fragment %d: n = %lld but synced n = %lld", p, (long long)n, (long long)f.n);
   if (f.gather != gather_buf)
     return ctx_fail(c, SD_ERR_ARG, "fragment %d: gather_buf %p is not the synced buffer %p", p, gather_buf, f.gather);
+  if ((st = check_alive(c))) return st;
   if (n > 0 && ((st = check_ptr(c, theta, 32, "theta")) || (st = check_ptr(c, anchor, 32, "anchor")) ||
                 (st = check_ptr(c, momentum, 32, "momentum"))))
     return st;
@@ -867,18 +900,17 @@ sd_status do_merge(sd_ctx* c, int32_t p, int64_t t, const void* gather_buf, floa
   const sdk::Payload pl = payload_of(&c->cfg, n);
   SD_CUDA(c, cudaSetDevice(c->device));
   SD_CUDA(c, cudaStreamWaitEvent(s, c->done[p], 0));  // block-receive (Alg. 2 L11)
-  if ((st = issue_push_wait(c, p, s))) return st;
+  if ((st = issue_round_wait(c, p, s))) return st;
   const uint8_t* payloads = static_cast<const uint8_t*>(gather_buf) + (f.push ? f.half_off : 0);
-  sdk::Pull pull;
-  if (f.pull) {
+  sdk::RoundRecv rr;
+  if (f.push) {
     GatherBuf* b = find_buf(c, gather_buf);
-    pull.win = b ? b->win : nullptr;
-    pull.half_off = f.half_off;
-    pull.rank = c->rank;
+    if (!b) return ctx_fail(c, SD_ERR_STATE, "fragment %d: push/pull-mode gather buffer not found", p);
+    rr = round_recv(c, f, b);
   }
   const int k = sdk::launch_apply(payloads, pl, c->M, theta, anchor, momentum, c->cfg.outer_lr,
                                   c->cfg.outer_momentum, c->cfg.alpha, c->status_dev, c->num_sms, s, inner,
-                                  f.pull ? &pull : nullptr);
+                                  f.push ? &rr : nullptr);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_apply launch");
   g_launches += (uint64_t)k;
   f = Inflight();
@@ -920,12 +952,19 @@ sd_status sd_check(sd_ctx* c, int64_t* first_bad_index) {
       return ctx_fail(c, SD_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(r != ncclSuccess ? r : ar));
   }
   volatile unsigned long long* h = c->status_host;
-  const unsigned long long flags = h[1], fb = h[0];
-  if (flags != 0) {
-    h[0] = ~0ull;
-    h[1] = 0;
+  const unsigned long long code = h[1], fb = h[0];
+  if (h[2] != 0) c->dead = true;
+  if (code != 0) {
+    if (code != 3) {  // a timeout stays reported (sticky)
+      h[0] = ~0ull;
+      h[1] = 0;
+    }
     if (first_bad_index) *first_bad_index = fb == ~0ull ? -1 : (int64_t)fb;
-    if (flags == 2) return ctx_fail(c, SD_ERR_STATE, "a gather slot had no valid payload trailer; round skipped");
+    if (code == 3)
+      return ctx_fail(c, SD_ERR_STATE,
+                      "a block-receive timed out (a peer missed its round flag for SD_WAIT_TIMEOUT_MS); the round "
+                      "was skipped here and this context refuses further device calls");
+    if (code == 2) return ctx_fail(c, SD_ERR_STATE, "a gather slot had no valid payload trailer; round skipped");
     return ctx_fail(c, SD_ERR_NONFINITE, "non-finite outer gradient at fragment index %llu; round skipped", fb);
   }
   return SD_OK;
@@ -939,10 +978,6 @@ sd_status sd_finalize(sd_ctx* c) {
   if (!c->bufs.empty()) cudaDeviceSynchronize();
   for (GatherBuf& b : c->bufs) release(c, b);
   c->bufs.clear();
-  if (c->mc) {
-    sdk::mc_destroy(c->comm, c->mc);
-    c->mc = nullptr;
-  }
   if (c->comm) {
     ncclCommDestroy(c->comm);
     c->comm = nullptr;
@@ -953,6 +988,9 @@ sd_status sd_finalize(sd_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->wb_stream) cudaStreamDestroy(c->wb_stream);
+  for (sd_ctx::Drain& d : c->drains)
+    if (d.ev) cudaEventDestroy(d.ev);
   for (cudaEvent_t e : c->staged)
     if (e) cudaEventDestroy(e);
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);

@@ -130,7 +130,6 @@ struct QArgs {
   int32_t lgB;      // log2(B), or -1 for one block per fragment
   uint8_t* slot;    // payload base
   size_t scales_off, trailer_off, bytes;
-  int64_t c_begin;  // first 1024-element chunk this launch handles (k_quantize tail after the TMA kernel)
   // fused all-gather (push mode): every payload word is also stored into the
   // same offset of this rank's slot in each peer's gather buffer (NVLink,
   // NCCL symmetric window, LSA pointers)
@@ -138,6 +137,13 @@ struct QArgs {
   ncclWindow_t win;
   size_t win_off;   // window offset of this rank's slot (same on every rank)
   int rank, M;
+  // round signal (push and pull modes) fused into the kernel's last CTA:
+  // {round id, first_bad} release-stored into entry `rank` of every peer's
+  // flag array (window offset flags_off); `counter` elects the last CTA
+  int sig;
+  size_t flags_off;
+  unsigned long long seq;
+  unsigned int* counter;
 };
 
 __device__ __forceinline__ void push_u32(const QArgs& a, size_t off, uint32_t v) {
@@ -147,6 +153,37 @@ __device__ __forceinline__ void push_u32(const QArgs& a, size_t off, uint32_t v)
 __device__ __forceinline__ void push_u8(const QArgs& a, size_t off, uint8_t v) {
   for (int q = 0; q < a.M; ++q)
     if (q != a.rank) *reinterpret_cast<uint8_t*>(ncclGetLsaPointer(a.win, a.win_off + off, q)) = v;
+}
+
+// Round signal, fused into the end of the kernel that finishes the payload
+// (DESIGN.md §7): every CTA, after its last store (bar.sync), takes a ticket
+// with an acquire-release atomic; the CTA that takes the last one has
+// observed every other CTA's payload writes (release/acquire chain through
+// the counter, cumulative over each CTA's barrier), so after a system-scope fence
+// its release-stores of {round id, first non-finite index} into each peer's
+// flag entry publish the whole payload to the peers' acquire loads.  In push
+// mode it also copies the first non-finite index into the peers' copies of
+// this rank's trailer.  The counter is reset for the next round (stream order).
+__device__ __forceinline__ void signal_round(const QArgs& a) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned int ticket;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(a.counter) : "memory");
+  if (ticket != gridDim.x - 1) return;
+  const unsigned long long fb = *reinterpret_cast<volatile unsigned long long*>(a.slot + a.trailer_off + 8);
+  *a.counter = 0u;
+  if (a.push)
+    for (int q = 0; q < a.M; ++q)
+      if (q != a.rank)
+        *reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.win_off + a.trailer_off + 8, q)) = fb;
+  __threadfence_system();
+  for (int q = 0; q < a.M; ++q) {
+    if (q == a.rank) continue;
+    unsigned long long* e =
+        reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.flags_off + 16 * (size_t)a.rank, q));
+    e[1] = fb;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(e), "l"(a.seq) : "memory");
+  }
 }
 
 // Chunk = 1024 elements = 4 rows of 256; lane `lane` owns elements
@@ -325,113 +362,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_quantize(QArgs a) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nfull = a.n >> 10;
-  for (int64_t c = a.c_begin + warp; c < nfull; c += nwarps) quantize_chunk<NB, true>(a, c, lane);
-  if ((nfull << 10) < a.n && warp == (nfull - a.c_begin) % nwarps) quantize_chunk<NB, false>(a, nfull, lane);
+  for (int64_t c = warp; c < nfull; c += nwarps) quantize_chunk<NB, true>(a, c, lane);
+  if ((nfull << 10) < a.n && warp == nfull % nwarps) quantize_chunk<NB, false>(a, nfull, lane);
   if (blockIdx.x == 0) write_tail(a);
-}
-
-// ---------------------------------------------------------------------------
-// k_quantize_tma: the same quantize with its input streams staged through
-// shared memory by the bulk-copy engine (cp.async.bulk, 1-D TMA) in a
-// kStages-deep mbarrier pipeline.  One producer warp per CTA issues the bulk
-// copies of a tile (kCW chunks of theta and of A, 2 x 32 KB); kCW consumer
-// warps each take one 1024-element chunk of the stage from shared memory and
-// run the unchanged block-max / encode / store path.  Persistent grid (one
-// CTA per SM); whole tiles only -- the remainder goes to k_quantize.
-// ---------------------------------------------------------------------------
-constexpr int kCW = 8;                       // consumer warps = chunks per tile
-constexpr int kStages = 3;
-constexpr int kTileBytes = kCW * 1024 * 4;   // per array
-constexpr int kTmaThreads = 32 * (kCW + 1);
-constexpr int kTmaSmem = kStages * 2 * kTileBytes + 2 * kStages * 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int NB>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_quantize_tma(QArgs a, int64_t ntiles) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  float* sth = reinterpret_cast<float*>(smem);                      // [kStages][kCW*1024]
-  float* san = reinterpret_cast<float*>(smem + kStages * kTileBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * kTileBytes);
-  uint64_t* empty = full + kStages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 0) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % kStages;
-        const uint32_t ph = (uint32_t)(it / kStages) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);  // slot free (first pass: passes at once)
-        mbar_expect_tx(&full[st], 2 * kTileBytes);
-        const int64_t e0 = tile * (kCW * 1024);
-        bulk_g2s(sth + st * (kCW * 1024), a.theta + e0, kTileBytes, &full[st]);
-        bulk_g2s(san + st * (kCW * 1024), a.anchor + e0, kTileBytes, &full[st]);
-      }
-    }
-    return;
-  }
-  const int cw = warp - 1;  // consumer index = chunk within the tile
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % kStages;
-    const uint32_t ph = (uint32_t)(it / kStages) & 1u;
-    mbar_wait(&full[st], ph);
-    const float* th = sth + st * (kCW * 1024) + cw * 1024 + 8 * lane;
-    const float* an = san + st * (kCW * 1024) + cw * 1024 + 8 * lane;
-    f8 d[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 t0 = *reinterpret_cast<const float4*>(th + 256 * k);
-      const float4 t1 = *reinterpret_cast<const float4*>(th + 256 * k + 4);
-      const float4 a0 = *reinterpret_cast<const float4*>(an + 256 * k);
-      const float4 a1 = *reinterpret_cast<const float4*>(an + 256 * k + 4);
-      d[k].v[0] = __fsub_rn(a0.x, t0.x);
-      d[k].v[1] = __fsub_rn(a0.y, t0.y);
-      d[k].v[2] = __fsub_rn(a0.z, t0.z);
-      d[k].v[3] = __fsub_rn(a0.w, t0.w);
-      d[k].v[4] = __fsub_rn(a1.x, t1.x);
-      d[k].v[5] = __fsub_rn(a1.y, t1.y);
-      d[k].v[6] = __fsub_rn(a1.z, t1.z);
-      d[k].v[7] = __fsub_rn(a1.w, t1.w);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // the stage's smem may be refilled
-    encode_block_rows<NB, true>(a, tile * kCW + cw, lane, d);
-  }
+  if (a.sig) signal_round(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -517,20 +451,46 @@ __global__ void __launch_bounds__(kThreads, 3) k_encode(QArgs a) {
     else encode_chunk<false>(a, c, lane);
   }
   if (blockIdx.x == 0) write_tail(a);
+  if (a.sig) signal_round(a);
 }
 
 // ---------------------------------------------------------------------------
-// Push-mode all-gather completion (fused into the quantize).
-// k_push_copy: two-pass quantize paths push the finished local slot (scales
-//   written by atomics) to every peer.
-// k_push_signal: after the pushing kernel, publish this rank's first
-//   non-finite index, fence at system scope, then release-store the round id
-//   (count of sends of the fragment, same on every rank) into flags[rank] of
-//   every peer.
-// k_push_wait: block-receive -- acquire-spin until every peer's flag holds it
-//   (bounded: on a timeout the missing peer's slot is marked invalid, the
-//   apply then skips the round and sd_check reports it).
+// Fused all-gather protocol (push and pull modes).
+// k_push_copy: the two-pass quantize paths push the finished local slot
+//   (scales written by atomics) to every peer, then signal the round.
+// k_round_wait: the block-receive (Alg. 2 L11).  One CTA decides the round
+//   once -- every peer's flag entry holds the round id (acquire, system
+//   scope), or, with a timeout configured (SD_WAIT_TIMEOUT_MS), a peer missed
+//   it -- and writes the verdict {first_bad, code} that the apply's CTAs read
+//   as plain stream-ordered data.  (Waiting in every apply CTA instead was
+//   measured slower: a system-scope acquire per CTA cost the apply 5% in push
+//   and 18% in pull mode at N = 2, profiles/r2_fused_wait_ab.txt.)
+// Verdict codes (also status[1]): 0 apply, 1 non-finite Delta somewhere,
+// 2 malformed own payload, 3 a peer missed the block-receive deadline (or
+// this context already had a timeout: sticky, status[2] = 1).
 // ---------------------------------------------------------------------------
+// k_signal: the round signal as its own one-thread kernel after the payload
+// kernel (push mode; see signal_kernel()): same stores as signal_round's last
+// CTA, ordered by the kernel boundary instead of the ticket counter.
+__global__ void k_signal(QArgs a) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long fb = *reinterpret_cast<volatile unsigned long long*>(a.slot + a.trailer_off + 8);
+  if (a.push)
+    for (int q = 0; q < a.M; ++q)
+      if (q != a.rank)
+        *reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.win_off + a.trailer_off + 8, q)) = fb;
+  __threadfence_system();
+  for (int q = 0; q < a.M; ++q) {
+    if (q == a.rank) continue;
+    unsigned long long* e =
+        reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.flags_off + 16 * (size_t)a.rank, q));
+    e[1] = fb;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(e), "l"(a.seq) : "memory");
+  }
+}
+
+constexpr unsigned long long kPeerTimedOut = 0xFFFFFFFFFFFFFFFEull;  // first_bad value a timed-out rank publishes
+
 __global__ void __launch_bounds__(kThreads) k_push_copy(QArgs a) {
   const size_t n16 = a.bytes / 16;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
@@ -538,44 +498,97 @@ __global__ void __launch_bounds__(kThreads) k_push_copy(QArgs a) {
     for (int q = 0; q < a.M; ++q)
       if (q != a.rank) *reinterpret_cast<uint4*>(ncclGetLsaPointer(a.win, a.win_off + 16 * i, q)) = v;
   }
+  if (a.sig) signal_round(a);
 }
 
-__global__ void k_push_signal(QArgs a, size_t flags_off, unsigned long long t) {
-  if (threadIdx.x != 0) return;
-  const unsigned long long fb = *reinterpret_cast<volatile unsigned long long*>(a.slot + a.trailer_off + 8);
-  for (int q = 0; q < a.M; ++q)
-    if (q != a.rank)
-      *reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, a.win_off + a.trailer_off + 8, q)) = fb;
-  __threadfence_system();
-  for (int q = 0; q < a.M; ++q) {
-    if (q == a.rank) continue;
-    unsigned long long* f =
-        reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(a.win, flags_off + 8 * (size_t)a.rank, q));
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(t) : "memory");
+struct WArgs {
+  const unsigned long long* flags;  // this half's flag entries {round id, first_bad} x M (local)
+  const uint8_t* own;               // this rank's own slot (local)
+  size_t trailer_off;
+  unsigned long long* verdict;      // {first_bad, code} (local)
+  int M, rank;
+  unsigned long long seq, timeout_ns;
+  volatile unsigned long long* status;  // host-mapped {first_bad, code, dead}
+  ncclWindow_t win;
+  size_t flags_off;                 // window offset of this half's flag array
+  int pull;                         // pull mode: check the slot addressing of the apply
+  size_t half_off, pb;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The own slot's trailer: its magic and first non-finite index (written by this
+// rank's own quantize earlier in stream order).
+__device__ __forceinline__ unsigned long long own_trailer_fb(const uint8_t* own, size_t trailer_off, int* bad) {
+  if (*reinterpret_cast<const uint32_t*>(own + trailer_off) != kMagic) *bad = 1;
+  return *reinterpret_cast<const unsigned long long*>(own + trailer_off + 8);
+}
+
+__global__ void k_round_wait(WArgs w) {
+  __shared__ unsigned long long s_fb;
+  __shared__ int s_code;
+  if (threadIdx.x == 0) {
+    s_fb = ~0ull;
+    s_code = w.status[2] ? 3 : 0;  // sticky: an earlier timeout on this context
   }
-}
-
-__global__ void k_push_wait(const unsigned long long* flags, uint8_t* half, size_t pb, size_t trailer_off, int M,
-                            int rank, unsigned long long t, unsigned long long timeout_ns,
-                            unsigned long long* status) {
+  __syncthreads();
   const int q = threadIdx.x;
-  if (q >= M || q == rank) return;
-  const unsigned long long t0 = globaltimer_ns();
-  unsigned long long v = 0;
-  while (true) {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
-    if (v == t) return;
-    if (globaltimer_ns() - t0 > timeout_ns) break;
-    __nanosleep(256);
+  if (q < w.M && s_code != 3) {
+    unsigned long long fb;
+    int code = 0;
+    if (w.pull) {  // the apply addresses slot m as LSA(half, 0) + m (LSA stride + pb): check it
+      const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off, 0));
+      const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off, 1));
+      const uint8_t* bq = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off + (size_t)q * w.pb, q));
+      if (bq != b0 + (size_t)q * ((size_t)(b1 - b0) + w.pb)) atomicMax(&s_code, 2);
+    }
+    if (q == w.rank) {
+      int bad = 0;
+      fb = own_trailer_fb(w.own, w.trailer_off, &bad);
+      if (bad) code = 2;
+    } else {
+      const unsigned long long t0 = globaltimer_ns();
+      bool ok = false;
+      while (true) {
+        if (ld_acquire_sys(w.flags + 2 * q) == w.seq) {
+          ok = true;
+          break;
+        }
+        if (w.timeout_ns && globaltimer_ns() - t0 > w.timeout_ns) break;
+        __nanosleep(128);
+      }
+      fb = ok ? w.flags[2 * q + 1] : ~0ull;
+      if (!ok || fb == kPeerTimedOut) code = 3;
+    }
+    if (code == 3 || fb == kPeerTimedOut) atomicMax(&s_code, 3);
+    else if (code) atomicMax(&s_code, code);
+    if (fb != kPeerTimedOut) atomicMin(&s_fb, fb);
   }
-  // invalidate the missing peer's local slot and this rank's own slot: the
-  // apply reads its own slot locally in every mode (the peers' slots are
-  // remote in pull mode), so a bad magic there makes it skip the round
-  *reinterpret_cast<volatile uint32_t*>(half + (size_t)q * pb + trailer_off) = 0u;
-  *reinterpret_cast<volatile uint32_t*>(half + (size_t)rank * pb + trailer_off) = 0u;
-  if (status) {
-    volatile unsigned long long* st = status;
-    st[1] = 2ull;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int code = s_code;
+  if (code == 0 && s_fb != ~0ull) code = 1;
+  w.verdict[0] = s_fb;
+  w.verdict[1] = (unsigned long long)code;
+  if (code == 0) return;
+  w.status[0] = s_fb;
+  w.status[1] = (unsigned long long)code;
+  if (code == 3 && !w.status[2]) {
+    // first timeout on this context: sticky from now on, and tell the peers
+    // (best effort) so that a peer that has not yet passed its own wait for
+    // this round skips it too
+    w.status[2] = 1ull;
+    __threadfence_system();
+    for (int p = 0; p < w.M; ++p) {
+      if (p == w.rank) continue;
+      unsigned long long* e =
+          reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(w.win, w.flags_off + 16 * (size_t)w.rank, p));
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(e + 1), "l"(kPeerTimedOut) : "memory");
+    }
   }
 }
 
@@ -678,6 +691,7 @@ __global__ void __launch_bounds__(kThreads) k_adamw_quantize(QArgs a, AdamArgs h
     encode_block_rows<NB, false>(a, nfull, lane, d);
   }
   if (blockIdx.x == 0) write_tail(a);
+  if (a.sig) signal_round(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -697,23 +711,33 @@ struct AArgs {
   float lr, mu, alpha, beta, invM;
   int pow2M;
   unsigned long long* status;
-  // pull mode: slot m lives in rank m's own buffer (symmetric window); the
-  // LSA mapping makes slot m = base0 + m * (peer stride + payload)
+  // push and pull modes: k_round_wait's verdict {first_bad, code} for this
+  // round; null in copy-engine mode (the CTAs read the local trailers)
+  const unsigned long long* verdict;
+  int rank;
+  // pull mode: slot m != rank is read from rank m's own buffer over NVLink
+  // (symmetric window; M <= 32, enforced by the host)
   int pull;
   ncclWindow_t win;
   size_t half_off;
 };
 
-__device__ __forceinline__ void slot_geometry(const AArgs& p, const uint8_t*& base, size_t& stride) {
-  if (p.pull) {
-    const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 0));
-    const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 1));
-    base = b0;
-    stride = (size_t)(b1 - b0) + p.pb;
-  } else {
-    base = p.gather;
-    stride = p.pb;
+// The round check every CTA makes before touching A, v, theta, by thread 0:
+// copy-engine mode reads the M trailers (local, L2-resident after the first
+// CTAs); push and pull modes read k_round_wait's verdict.  -> code (0 apply,
+// 1 non-finite, 2 malformed, 3 timeout) and the smallest first_bad.
+__device__ __forceinline__ int round_check(const AArgs& p, int M, unsigned long long& fb) {
+  if (p.verdict) {
+    fb = p.verdict[0];
+    return (int)p.verdict[1];
   }
+  int bad = 0;
+  fb = ~0ull;
+  for (int q = 0; q < M; ++q) {
+    const unsigned long long f = own_trailer_fb(p.gather + (size_t)q * p.pb, p.trailer_off, &bad);
+    fb = f < fb ? f : fb;
+  }
+  return bad ? 2 : (fb != ~0ull ? 1 : 0);
 }
 
 // Decodes 8 codes (nibble i = element i) into LUT values +-2^(e-7) (codes 0
@@ -758,29 +782,38 @@ template <int kM, bool kAdam>
 #endif
 __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_ADAM8 : SD_APPLY_MINB)
     k_apply(AArgs p, AdamArgs h) {
-  __shared__ int skip;
+  __shared__ int s_skip;
   const int M = kM > 0 ? kM : p.M;
-  const uint8_t* gbase;
-  size_t gstride;
-  slot_geometry(p, gbase, gstride);
+  // one barrier (each CTA is short-lived: a second one measured 2.5% slower)
   if (threadIdx.x == 0) {
-    unsigned long long fb = ~0ull;
-    int badmagic = 0;
-    for (int m = 0; m < M; ++m) {
-      const uint8_t* tr = gbase + (size_t)m * gstride + p.trailer_off;
-      if (*reinterpret_cast<const uint32_t*>(tr) != kMagic) badmagic = 1;
-      const unsigned long long f = *reinterpret_cast<const unsigned long long*>(tr + 8);
-      fb = f < fb ? f : fb;
-    }
-    skip = badmagic || fb != ~0ull;
-    if (skip && blockIdx.x == 0 && p.status) {
+    unsigned long long fb;
+    const int code = round_check(p, M, fb);
+    s_skip = code != 0;
+    if (code && blockIdx.x == 0 && p.status && !p.verdict) {
       volatile unsigned long long* st = p.status;
       st[0] = fb;
-      st[1] = badmagic ? 2ull : 1ull;
+      st[1] = (unsigned long long)code;
     }
   }
   __syncthreads();
-  if (skip && !kAdam) return;  // poisoned round: nothing changes (with kAdam the inner step still runs)
+  const bool skip = s_skip;
+  if (skip && !kAdam) return;  // skipped round: nothing changes (with kAdam the inner step still runs)
+  // slot m's base address.  Pull mode: slot m of rank m's buffer through the
+  // window's NVLink (LSA) mapping, ncclGetLsaPointer(win, half_off + m pb, m)
+  // = LSA(half_off, 0) + m (LSA stride + pb) -- the flat per-peer layout of
+  // the LSA window; k_round_wait checks that identity for every peer of
+  // every round before the apply may run.  Kept in registers: reading the M
+  // addresses from shared memory instead measured 4% slower
+  // (profiles/r2_pull_ab.txt).
+  const uint8_t* gb = p.gather;
+  size_t gs = p.pb;
+  if (p.pull) {
+    const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 0));
+    const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 1));
+    gb = b0;
+    gs = (size_t)(b1 - b0) + p.pb;
+  }
+  auto slot_of = [&](int m) -> const uint8_t* { return gb + (size_t)m * gs; };
 
   const int64_t n8 = p.n >> 3;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -793,12 +826,12 @@ __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_A
     if (kM > 0 && !(kAdam && skip)) {
 #pragma unroll
       for (int m = 0; m < kMr; ++m) {
-        const uint8_t* slot = gbase + (size_t)m * gstride;
+        const uint8_t* slot = slot_of(m);
         code[m] = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
         scl[m] = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
       }
     }
-    f8 t = kAdam ? ld8(p.theta + 8 * i) : ld8_stream(p.theta + 8 * i);
+    f8 t = ld8(p.theta + 8 * i);  // coherent load: this kernel writes theta
     if (kAdam) {  // the inner step of this step first (Alg. 2 L5 precedes L10-13)
       const f8 g = ld8_stream(h.grad + 8 * i);
       f8 m1 = ld8(h.m + 8 * i), m2 = ld8(h.v + 8 * i);
@@ -822,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_A
         cw = code[m];
         s = scl[m];
       } else {
-        const uint8_t* slot = gbase + (size_t)m * gstride;
+        const uint8_t* slot = slot_of(m);
         cw = ld_code_word(reinterpret_cast<const uint32_t*>(slot) + i);
         s = __ldg(reinterpret_cast<const float*>(slot + p.scales_off) + blk);
       }
@@ -854,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_A
     const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
     float S = 0.0f;
     for (int m = 0; m < M; ++m) {
-      const uint8_t* slot = gbase + (size_t)m * gstride;
+      const uint8_t* slot = slot_of(m);
       const uint32_t c = (slot[e >> 1] >> ((e & 1) * 4)) & 15u;
       float q[8];
       decode8(c, reinterpret_cast<const float*>(slot + p.scales_off)[blk], q);
@@ -866,154 +899,6 @@ __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_A
     p.v[e] = w;
     p.theta[e] = t;
   }
-}
-
-// ---------------------------------------------------------------------------
-// k_apply_tma: k_apply with a tile's A, v, theta and M code chunks staged
-// through shared memory by 1-D bulk copies (cp.async.bulk) in a
-// kAStages-deep mbarrier ring: one producer warp, kAW consumer warps (two
-// 256-element rows each), results stored directly with 256-bit stores.
-// Persistent grid (one CTA per SM), whole tiles only -- launch_apply hands
-// the rest to k_apply.  The north star's "staged through shared memory/TMA"
-// design, kept as a measured alternative (SD_APPLY_TMA=1); same arithmetic
-// (decode8 + ascending-m sum + outer_step), so bit-identical to k_apply.
-// ---------------------------------------------------------------------------
-#ifndef SD_ATMA_STAGES
-#define SD_ATMA_STAGES 2  // best of the measured configurations (profiles/atma_ab_r1.txt)
-#endif
-#ifndef SD_ATMA_CTAS
-#define SD_ATMA_CTAS 1  // CTAs per SM
-#endif
-constexpr int kAW = 8;                  // consumer warps
-constexpr int kATile = kAW * 512;       // elements per tile
-constexpr int kAStages = SD_ATMA_STAGES;
-constexpr int kATmaThreads = 32 * (kAW + 1);
-template <int kM>
-struct ApplyTmaLayout {
-  static constexpr int kArr = 4 * kATile;                      // bytes of A (or v, theta) per stage
-  static constexpr int kCodes = kATile / 2;                    // code bytes per slot per stage
-  static constexpr int kStage = 3 * kArr + kM * kCodes;
-  static constexpr int kSmem = kAStages * kStage + 2 * kAStages * 8;
-};
-
-template <int kM>
-__global__ void __launch_bounds__(kATmaThreads, SD_ATMA_CTAS) k_apply_tma(AArgs p, int64_t ntiles) {
-  using L = ApplyTmaLayout<kM>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAStages * L::kStage);
-  uint64_t* empty = full + kAStages;
-  __shared__ int skip;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint8_t* gbase = p.gather;
-  const size_t gstride = p.pb;
-  if (threadIdx.x == 0) {
-    unsigned long long fb = ~0ull;
-    int badmagic = 0;
-    for (int m = 0; m < kM; ++m) {
-      const uint8_t* tr = gbase + (size_t)m * gstride + p.trailer_off;
-      if (*reinterpret_cast<const uint32_t*>(tr) != kMagic) badmagic = 1;
-      const unsigned long long f = *reinterpret_cast<const unsigned long long*>(tr + 8);
-      fb = f < fb ? f : fb;
-    }
-    skip = badmagic || fb != ~0ull;
-    if (skip && blockIdx.x == 0 && p.status) {
-      volatile unsigned long long* st = p.status;
-      st[0] = fb;
-      st[1] = badmagic ? 2ull : 1ull;
-    }
-    for (int s = 0; s < kAStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kAW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (skip) return;
-  if (warp == 0) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % kAStages;
-        const uint32_t ph = (uint32_t)(it / kAStages) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);
-        mbar_expect_tx(&full[st], L::kStage);
-        uint8_t* sb = smem + st * L::kStage;
-        const int64_t e0 = tile * kATile;
-        bulk_g2s(sb, p.A + e0, L::kArr, &full[st]);
-        bulk_g2s(sb + L::kArr, p.v + e0, L::kArr, &full[st]);
-        bulk_g2s(sb + 2 * L::kArr, p.theta + e0, L::kArr, &full[st]);
-#pragma unroll
-        for (int m = 0; m < kM; ++m)
-          bulk_g2s(sb + 3 * L::kArr + m * L::kCodes, gbase + (size_t)m * gstride + e0 / 2, L::kCodes, &full[st]);
-      }
-    }
-    return;
-  }
-  const int cw = warp - 1;
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % kAStages;
-    const uint32_t ph = (uint32_t)(it / kAStages) & 1u;
-    mbar_wait(&full[st], ph);
-    const uint8_t* sb = smem + st * L::kStage;
-#pragma unroll 1
-    for (int r = 0; r < 2; ++r) {  // one 256-element row at a time: 24 floats + M code words live
-      const int le = cw * 512 + r * 256 + 8 * lane;
-      const float* sa = reinterpret_cast<const float*>(sb) + le;
-      const float* sv = reinterpret_cast<const float*>(sb + L::kArr) + le;
-      const float* stt = reinterpret_cast<const float*>(sb + 2 * L::kArr) + le;
-      f8 a, w, t;
-#pragma unroll
-      for (int j = 0; j < 8; j += 4) {
-        const float4 x = *reinterpret_cast<const float4*>(sa + j);
-        const float4 y = *reinterpret_cast<const float4*>(sv + j);
-        const float4 z = *reinterpret_cast<const float4*>(stt + j);
-        a.v[j] = x.x; a.v[j + 1] = x.y; a.v[j + 2] = x.z; a.v[j + 3] = x.w;
-        w.v[j] = y.x; w.v[j + 1] = y.y; w.v[j + 2] = y.z; w.v[j + 3] = y.w;
-        t.v[j] = z.x; t.v[j + 1] = z.y; t.v[j + 2] = z.z; t.v[j + 3] = z.w;
-      }
-      uint32_t code[kM];
-#pragma unroll
-      for (int m = 0; m < kM; ++m) code[m] = *reinterpret_cast<const uint32_t*>(sb + 3 * L::kArr + m * L::kCodes + le / 2);
-      const int64_t e = tile * kATile + le;
-      const int64_t blk = p.lgB < 0 ? 0 : (e >> p.lgB);
-      float S[8];
-#pragma unroll
-      for (int m = 0; m < kM; ++m) {
-        const float sc = __ldg(reinterpret_cast<const float*>(gbase + (size_t)m * gstride + p.scales_off) + blk);
-        float q[8];
-        decode8(code[m], sc, q);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) S[j] = (m == 0) ? q[j] : __fadd_rn(S[j], q[j]);  // ascending m
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) outer_step(S[j], a.v[j], w.v[j], t.v[j], p);
-      st8(p.A + e, a);
-      st8(p.v + e, w);
-      st8(p.theta + e, t);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // the stage may be refilled
-  }
-}
-
-bool use_tma_apply() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SD_APPLY_TMA");
-    v = (e && atoi(e) == 1) ? 1 : 0;
-  }
-  return v == 1;
-}
-
-template <int kM>
-void launch_apply_tma(const AArgs& p, int64_t ntiles, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_apply_tma<kM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ApplyTmaLayout<kM>::kSmem);
-    attr = true;
-  }
-  k_apply_tma<kM><<<grid, kATmaThreads, ApplyTmaLayout<kM>::kSmem, st>>>(p, ntiles);
 }
 
 int ilog2_or_neg(int32_t B) {
@@ -1049,7 +934,21 @@ int grid_for(K kernel, int num_sms, int64_t work_items, int items_per_block) {
 }  // namespace
 
 namespace {
-QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Push& push) {
+// Round-signal form: fused into the payload kernel's last CTA, or a separate
+// one-thread kernel after it.  Measured at N = 2 and 4 (profiles/r2_pull_ab.txt):
+// equal for pull; for push the fused form costs the quantize ~6% (its CTAs
+// linger on the release ticket until their NVLink stores complete), so push
+// signals from its own kernel.  SD_SIGNAL_KERNEL=0|1 forces one form.
+bool signal_kernel(bool push) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SD_SIGNAL_KERNEL");
+    v = e ? (atoi(e) == 1 ? 1 : 0) : -1;
+  }
+  return v >= 0 ? v == 1 : push;
+}
+
+QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Round& rd) {
   QArgs a;
   a.theta = theta;
   a.anchor = anchor;
@@ -1060,150 +959,82 @@ QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uin
   a.scales_off = pl.scales_off;
   a.trailer_off = pl.trailer_off;
   a.bytes = pl.bytes;
-  a.c_begin = 0;
-  a.push = push.win != nullptr;
-  a.win = push.win;
-  a.win_off = push.win_off;
-  a.rank = push.rank;
-  a.M = push.M;
+  a.push = rd.win != nullptr && rd.push;
+  a.win = rd.win;
+  a.win_off = rd.win_off;
+  a.rank = rd.rank;
+  a.M = rd.M;
+  a.sig = rd.win != nullptr && !signal_kernel(rd.push);
+  a.flags_off = rd.flags_off;
+  a.seq = (unsigned long long)rd.seq;
+  a.counter = rd.counter;
   return a;
 }
 
 bool single_pass(int32_t B) { return B == 256 || B == 512 || B == 1024; }
 
-// SD_QUANTIZE_TMA=1 stages the quantize's input streams through shared memory
-// with bulk copies (k_quantize_tma); default: direct 256-bit loads.
-bool use_tma_quantize() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SD_QUANTIZE_TMA");
-    v = (e && atoi(e) == 1) ? 1 : 0;
-  }
-  return v == 1;
-}
-
-template <int NB>
-void launch_tma(const QArgs& a, int64_t ntiles, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_quantize_tma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    attr = true;
-  }
-  k_quantize_tma<NB><<<grid, kTmaThreads, kTmaSmem, st>>>(a, ntiles);
-}
-}  // namespace
-
-int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Push& push,
-                    int num_sms, cudaStream_t st) {
-  const QArgs a = make_qargs(theta, anchor, pl, slot, push);
-  const int64_t chunks = (pl.n + 1023) >> 10;
-  const int wpb = kThreads / 32;
-  int launched = 0;
-  if (single_pass(pl.B)) {
-    QArgs t = a;
-    const int64_t ntiles = use_tma_quantize() ? (pl.n >> 10) / kCW : 0;
-    if (ntiles > 0) {  // whole tiles through the bulk-copy pipeline, the rest below
-      const int g = (int)(ntiles < num_sms ? ntiles : num_sms);
-      if (pl.B == 1024) launch_tma<1>(a, ntiles, g, st);
-      else if (pl.B == 512) launch_tma<2>(a, ntiles, g, st);
-      else launch_tma<4>(a, ntiles, g, st);
-      t.c_begin = ntiles * kCW;
-      ++launched;
-    }
-    const int64_t rest = chunks - t.c_begin > 0 ? chunks - t.c_begin : 1;  // >= 1 CTA: write_tail
-    if (pl.B == 1024) k_quantize<1><<<grid_for(k_quantize<1>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
-    else if (pl.B == 512) k_quantize<2><<<grid_for(k_quantize<2>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
-    else k_quantize<4><<<grid_for(k_quantize<4>, num_sms, rest, wpb), kThreads, 0, st>>>(t);
-    ++launched;
-  } else {
-    QArgs loc = a;
-    loc.push = 0;  // scales come from atomics: build locally, then push the finished slot
-    if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
-    k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
-    k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
-    launched = 2;
-    if (a.push) {
-      k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
-      launched = 3;
-    }
-  }
-  return cudaGetLastError() == cudaSuccess ? launched : -1;
-}
-
-int launch_push_signal(const Payload& pl, uint8_t* slot, const Push& push, size_t flags_off, uint64_t t,
-                       cudaStream_t st) {
-  const QArgs a = make_qargs(nullptr, nullptr, pl, slot, push);
-  k_push_signal<<<1, 32, 0, st>>>(a, flags_off, (unsigned long long)t);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
-}
-
-// ---------------------------------------------------------------------------
-// Multicast gather support (NVLS through the NCCL device API).
-// ---------------------------------------------------------------------------
-struct McState {
-  ncclDevComm_t dc;
-  void** host_ptr = nullptr;  // mapped pinned word for mc_base
-};
-
-namespace {
-__global__ void k_mc_base(ncclWindow_t w, ncclMultimemHandle mm, void** out) {
-  *out = ncclGetMultimemPointer(w, 0, mm);
-}
-__global__ void k_flag_signal(ncclWindow_t w, size_t flags_off, int rank, int M, unsigned long long t) {
-  if (threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int q = 0; q < M; ++q) {
-    if (q == rank) continue;
-    unsigned long long* f = reinterpret_cast<unsigned long long*>(ncclGetLsaPointer(w, flags_off + 8 * (size_t)rank, q));
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(t) : "memory");
-  }
-}
-}  // namespace
-
-int mc_create(ncclComm_t comm, McState** out) {
-  *out = nullptr;
-  McState* s = new McState();
-  ncclDevCommRequirements_t req = {};
-  req.lsaMultimem = true;
-  if (ncclDevCommCreate(comm, &req, &s->dc) != ncclSuccess) {
-    delete s;
-    return -1;
-  }
-  if (s->dc.lsaMultimem.mcBasePtr == nullptr ||
-      cudaHostAlloc(reinterpret_cast<void**>(&s->host_ptr), sizeof(void*), cudaHostAllocMapped) != cudaSuccess) {
-    ncclDevCommDestroy(comm, &s->dc);
-    delete s;
-    return 0;
-  }
-  *out = s;
+// the separate-kernel form of the round signal (SD_SIGNAL_KERNEL=1)
+int maybe_signal(const Round& rd, const QArgs& a, cudaStream_t st) {
+  if (!rd.win || !signal_kernel(rd.push)) return 0;
+  QArgs s = a;
+  s.push = rd.push;
+  k_signal<<<1, 32, 0, st>>>(s);
   return 1;
 }
 
-void mc_destroy(ncclComm_t comm, McState* s) {
-  if (!s) return;
-  ncclDevCommDestroy(comm, &s->dc);
-  if (s->host_ptr) cudaFreeHost(s->host_ptr);
-  delete s;
+}  // namespace
+
+int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Round& rd,
+                    int num_sms, cudaStream_t st) {
+  const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
+  const int64_t chunks = (pl.n + 1023) >> 10;
+  const int wpb = kThreads / 32;
+  if (single_pass(pl.B)) {
+    const int g = grid_for(k_quantize<1>, num_sms, chunks > 0 ? chunks : 1, wpb);  // >= 1 CTA: write_tail
+    if (pl.B == 1024) k_quantize<1><<<g, kThreads, 0, st>>>(a);
+    else if (pl.B == 512) k_quantize<2><<<g, kThreads, 0, st>>>(a);
+    else k_quantize<4><<<g, kThreads, 0, st>>>(a);
+    const int ks = maybe_signal(rd, a, st);
+    return cudaGetLastError() == cudaSuccess ? 1 + ks : -1;
+  }
+  // two passes: the scales come from atomics, so the slot is built locally;
+  // in push mode the finished slot is then pushed (and the round signalled) by k_push_copy
+  QArgs loc = a;
+  loc.push = 0;
+  loc.sig = a.sig && !a.push;
+  if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
+  QArgs pass1 = loc;
+  pass1.sig = 0;
+  k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1);
+  k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
+  int launched = 2;
+  if (a.push) {
+    k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
+    launched = 3;
+  }
+  launched += maybe_signal(rd, a, st);
+  return cudaGetLastError() == cudaSuccess ? launched : -1;
 }
 
-int mc_base(McState* s, ncclWindow_t win, uint8_t** out, cudaStream_t st) {
-  void** dev = nullptr;
-  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), s->host_ptr, 0) != cudaSuccess) return -1;
-  k_mc_base<<<1, 1, 0, st>>>(win, s->dc.lsaMultimem, dev);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return -1;
-  *out = static_cast<uint8_t*>(*reinterpret_cast<void* volatile*>(s->host_ptr));
-  return *out ? 1 : -1;
-}
-
-int launch_flag_signal(ncclWindow_t win, size_t flags_off, int rank, int M, uint64_t t, cudaStream_t st) {
-  k_flag_signal<<<1, 32, 0, st>>>(win, flags_off, rank, M, (unsigned long long)t);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
-}
-
-int launch_push_wait(const unsigned long long* flags, uint8_t* half, const Payload& pl, int M, int rank, uint64_t t,
-                     uint64_t timeout_ns, unsigned long long* status, cudaStream_t st) {
-  k_push_wait<<<1, 32, 0, st>>>(flags, half, pl.bytes, pl.trailer_off, M, rank, (unsigned long long)t,
-                                (unsigned long long)timeout_ns, status);
+int launch_round_wait(const RoundRecv& rr, const Payload& pl, int M, uint64_t timeout_ns, unsigned long long* status,
+                      cudaStream_t st) {
+  WArgs w;
+  w.flags = rr.flags;
+  w.own = rr.own;
+  w.trailer_off = pl.trailer_off;
+  w.verdict = rr.verdict;
+  w.M = M;
+  w.rank = rr.rank;
+  w.seq = (unsigned long long)rr.seq;
+  w.timeout_ns = (unsigned long long)timeout_ns;
+  w.status = status;
+  w.win = rr.win;
+  w.flags_off = rr.flags_off;
+  w.pull = rr.pull;
+  w.half_off = rr.half_off;
+  w.pb = pl.bytes;
+  const int threads = 32 * ((M + 31) / 32);
+  k_round_wait<<<1, threads, 0, st>>>(w);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -1236,29 +1067,30 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 }
 
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
-                          uint8_t* slot, const AdamHyper& hp, const Push& push, int num_sms, cudaStream_t st) {
+                          uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st) {
   if (!single_pass(pl.B)) {  // two-pass scales: AdamW, then quantize
     const int k1 = launch_adamw(theta, grad, m, v, pl.n, hp, num_sms, st);
     if (k1 < 0) return -1;
-    const int k2 = launch_quantize(theta, anchor, pl, slot, push, num_sms, st);
+    const int k2 = launch_quantize(theta, anchor, pl, slot, rd, num_sms, st);
     return k2 < 0 ? -1 : k1 + k2;
   }
-  const QArgs a = make_qargs(theta, anchor, pl, slot, push);
+  const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
   const AdamArgs h = make_adam(theta, grad, m, v, pl.n, hp);
   const int64_t chunks = (pl.n + 1023) >> 10;
-  const int wpb = kThreads / 32;
+  const int g = grid_for(k_adamw_quantize<1>, num_sms, chunks > 0 ? chunks : 1, kThreads / 32);
   if (pl.B == 1024)
-    k_adamw_quantize<1><<<grid_for(k_adamw_quantize<1>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
+    k_adamw_quantize<1><<<g, kThreads, 0, st>>>(a, h);
   else if (pl.B == 512)
-    k_adamw_quantize<2><<<grid_for(k_adamw_quantize<2>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
+    k_adamw_quantize<2><<<g, kThreads, 0, st>>>(a, h);
   else
-    k_adamw_quantize<4><<<grid_for(k_adamw_quantize<4>, num_sms, chunks, wpb), kThreads, 0, st>>>(a, h);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+    k_adamw_quantize<4><<<g, kThreads, 0, st>>>(a, h);
+  const int ks = maybe_signal(rd, a, st);
+  return cudaGetLastError() == cudaSuccess ? 1 + ks : -1;
 }
 
 int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, float* anchor, float* momentum,
                  float lr, float mu, float alpha, unsigned long long* status, int num_sms, cudaStream_t st,
-                 const AdamInner* inner, const Pull* pull) {
+                 const AdamInner* inner, const RoundRecv* rr) {
   AArgs p;
   p.gather = gather;
   p.pb = pl.bytes;
@@ -1277,48 +1109,20 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
   p.pow2M = (M & (M - 1)) == 0;
   p.invM = 1.0f / (float)M;  // exact when M is a power of two
   p.status = status;
-  p.pull = pull != nullptr && pull->win != nullptr;
-  p.win = p.pull ? pull->win : nullptr;
-  p.half_off = p.pull ? pull->half_off : 0;
+  p.verdict = rr ? rr->verdict : nullptr;
+  p.rank = rr ? rr->rank : 0;
+  p.pull = rr != nullptr && rr->pull;
+  p.win = rr ? rr->win : nullptr;
+  p.half_off = rr ? rr->half_off : 0;
   AdamArgs h{};
   if (inner) h = make_adam(theta, inner->grad, inner->m, inner->v, pl.n, inner->hp);
-  int launched = 0;
-  // SD_APPLY_TMA=1: whole tiles through the bulk-copy pipeline (local slots,
-  // no inner step, B a divisor of the tile), the rest through k_apply below
-  const int64_t ntiles = (use_tma_apply() && !inner && !p.pull && (M == 1 || M == 2 || M == 4 || M == 8) &&
-                          (pl.B == 0 || (pl.B >= 256 && pl.B <= kATile)))
-                             ? pl.n / kATile
-                             : 0;
-  if (ntiles > 0) {
-#ifdef SD_ATMA_ONESHOT
-    const int64_t cap = ntiles;  // one CTA per tile
-#else
-    const int64_t cap = (int64_t)num_sms * SD_ATMA_CTAS;
-#endif
-    const int g = (int)(ntiles < cap ? ntiles : cap);
-    switch (M) {
-      case 1: launch_apply_tma<1>(p, ntiles, g, st); break;
-      case 2: launch_apply_tma<2>(p, ntiles, g, st); break;
-      case 4: launch_apply_tma<4>(p, ntiles, g, st); break;
-      default: launch_apply_tma<8>(p, ntiles, g, st); break;
-    }
-    ++launched;
-    const int64_t off = ntiles * kATile;  // a multiple of B: shift every stream to the rest
-    p.A += off;
-    p.v += off;
-    p.theta += off;
-    p.n -= off;
-    p.gather += off / 2;
-    p.scales_off = p.scales_off - (size_t)(off / 2) + (p.lgB < 0 ? 0 : 4 * (size_t)(off >> p.lgB));
-    p.trailer_off -= (size_t)(off / 2);
-    if (p.n == 0) return cudaGetLastError() == cudaSuccess ? launched : -1;
-  }
   const int64_t items = (p.n >> 3) > 0 ? (p.n >> 3) : 1;
-#define SD_APPLY_CASE(KM)                                                                                         \
-  if (inner)                                                                                                      \
-    k_apply<KM, true><<<grid_for(k_apply<KM, true>, num_sms, items, kThreads), kThreads, 0, st>>>(p, h);          \
-  else                                                                                                            \
-    k_apply<KM, false><<<grid_for(k_apply<KM, false>, num_sms, items, kThreads), kThreads, 0, st>>>(p, h);
+  const int g = grid_for(k_apply<1, false>, num_sms, items, kThreads);
+#define SD_APPLY_CASE(KM)                                     \
+  if (inner)                                                  \
+    k_apply<KM, true><<<g, kThreads, 0, st>>>(p, h);          \
+  else                                                        \
+    k_apply<KM, false><<<g, kThreads, 0, st>>>(p, h);
   switch (M) {
     case 1: SD_APPLY_CASE(1) break;
     case 2: SD_APPLY_CASE(2) break;
@@ -1327,7 +1131,7 @@ int launch_apply(const uint8_t* gather, const Payload& pl, int M, float* theta, 
     default: SD_APPLY_CASE(0) break;
   }
 #undef SD_APPLY_CASE
-  return cudaGetLastError() == cudaSuccess ? launched + 1 : -1;
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace sdk

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("SD_LIBSD") or os.path.join(_HERE, "libsd.so")  # over
 SD_ABI_VERSION = 1
 SD_UNIQUE_ID_BYTES = 128
 SD_PAYLOAD_MAGIC = 0x31304453
-SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH, SD_GATHER_AUTO, SD_GATHER_PULL, SD_GATHER_MULTICAST = 0, 1, 2, 3, 4
+SD_GATHER_COPY_ENGINE, SD_GATHER_PUSH, SD_GATHER_AUTO, SD_GATHER_PULL = 0, 1, 2, 3
 
 SD_OK, SD_ERR_ARG, SD_ERR_CONFIG, SD_ERR_SCHEDULE, SD_ERR_STATE, SD_ERR_NONFINITE, SD_ERR_CUDA, SD_ERR_NCCL = range(8)
 STATUS_NAMES = {
@@ -29,7 +29,7 @@ EXPORTS = (
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free", "sd_set_gather_mode",
     "sd_gather_payloads",
-    "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync",
+    "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync", "sd_comm_stream",
     "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_inner_adamw_merge", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
@@ -89,6 +89,7 @@ def lib():
             "sd_state_prefetch": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_sync": ([P, P], I32),
+            "sd_comm_stream": ([P, ctypes.POINTER(P)], I32),
             "sd_outer_grad_quantize": ([P, I32, I64, P, P, I64, P, P], I32),
             "sd_inner_adamw": ([P, I64, P, P, P, P, I64, ctypes.POINTER(SdAdamW), P], I32),
             "sd_inner_adamw_quantize": ([P, I32, I64, I64, P, P, P, P, P, I64, P, ctypes.POINTER(SdAdamW), P], I32),
@@ -266,6 +267,12 @@ class SdContext:
 
     def sd_state_sync(self, stream=None):
         self._c(lib().sd_state_sync(self.h, _stream(stream)))
+
+    def sd_comm_stream(self) -> int:
+        """cudaStream_t handle (int) of the ctx's comm stream, for tracing (torch.cuda.ExternalStream)."""
+        out = ctypes.c_void_p(0)
+        self._c(lib().sd_comm_stream(self.h, ctypes.byref(out)))
+        return out.value or 0
 
     def sd_outer_state_init(self, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n

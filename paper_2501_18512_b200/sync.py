@@ -33,16 +33,10 @@ class FragmentSync:
         # libsd-owned gather buffers: NCCL symmetric memory (copy-engine all-gather, zero SMs)
         # with a communicator; plain device memory otherwise
         self.gather = []
-        for n, pb in zip(self.n, self.payload):
-            try:
-                self.gather.append(self.ctx.sd_gather_alloc(n))
-            except sd.SdError as e:  # no symmetric memory here: caller-owned buffer, NCCL SM-kernel gather
-                import sys
-
-                import torch
-
-                print(f"[FragmentSync] sd_gather_alloc failed ({e}); using a plain device buffer", file=sys.stderr)
-                self.gather.append(torch.empty(world * pb, dtype=torch.uint8, device=torch.device("cuda", device)))
+        for n in self.n:
+            # collective with a communicator (every rank allocates in the same order): a failure
+            # here must not be papered over on one rank, or the ranks would run different protocols
+            self.gather.append(self.ctx.sd_gather_alloc(n))
 
     def slot(self, p: int) -> torch.Tensor:
         pb = self.payload[p]

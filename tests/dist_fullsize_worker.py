@@ -43,7 +43,7 @@ def main():
     segs_all = [wl.segments(blocks, emb) for blocks, _, emb in layout]
     segs = segs_all[p]
     n = synth.segments_numel(segs)
-    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL, "mc": sd.SD_GATHER_MULTICAST,
+    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL,
             "ce": sd.SD_GATHER_COPY_ENGINE}.get(os.environ.get("SD_TEST_GATHER"), sd.SD_GATHER_AUTO)
     fsync = FragmentSync(cfg, [synth.segments_numel(s) for s in segs_all], rank, world, local, gather_mode=mode)
     A = synth.dev_init(torch.empty(n, device=dev), segs, p)

@@ -1,5 +1,5 @@
 """Worker for tests/test_gpu_multi.py: the fused inner-step calls on real
-NCCL ranks, in every gather mode (SD_TEST_GATHER = ce | push | pull | mc).
+NCCL ranks, in every gather mode (SD_TEST_GATHER = ce | push | pull).
 
 Per round, on every rank (replica m = rank):
   send step   sd_inner_adamw_quantize  (AdamW + Delta + E3M0 in one kernel;
@@ -42,7 +42,7 @@ def main():
     P = sd.sd_fragment_count(cfg)
     p = 1
     t_p = sd.sd_fragment_layout(cfg, p)[1]
-    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL, "mc": sd.SD_GATHER_MULTICAST}.get(
+    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}.get(
         os.environ.get("SD_TEST_GATHER"), sd.SD_GATHER_COPY_ENGINE)
     fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode)
     ctx = fsync.ctx

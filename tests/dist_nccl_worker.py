@@ -37,7 +37,7 @@ def main():
     P = sd.sd_fragment_count(cfg)
     p = 2
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)
-    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL, "mc": sd.SD_GATHER_MULTICAST}.get(
+    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}.get(
         os.environ.get("SD_TEST_GATHER"), sd.SD_GATHER_COPY_ENGINE)
     fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode)
     if os.environ.get("SD_TEST_TORCH_BUF") == "1":  # caller-owned (non-symmetric) gather buffers

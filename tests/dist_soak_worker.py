@@ -33,7 +33,7 @@ def main():
     layout = [sd.sd_fragment_layout(cfg, q) for q in range(P)]
     segs = [wl.segments(b, e) for b, _, e in layout]
     n = [synth.segments_numel(s) for s in segs]
-    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL, "mc": sd.SD_GATHER_MULTICAST,
+    mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL,
             "ce": sd.SD_GATHER_COPY_ENGINE}[os.environ["SD_TEST_GATHER"]]
     fsync = FragmentSync(cfg, n, rank, world, local, gather_mode=mode)
     A = [synth.dev_init(torch.empty(k, device=dev), s, p) for p, (k, s) in enumerate(zip(n, segs))]

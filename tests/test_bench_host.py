@@ -46,3 +46,25 @@ def test_overrides():
     args = argparse.Namespace(tau=0, fragment_size=6)
     wl = bench.workload_with_overrides(WORKLOADS["1B"], args)
     assert wl.tau == 0 and wl.fragment_size == 6 and WORKLOADS["1B"].tau == 5
+
+
+def test_reference_arm_uses_only_the_oracle():
+    """`bench.py --impl reference` takes its calendar and fragment layout from
+    the oracle's own scheduler (identical to libsd's) and never loads libsd."""
+    import subprocess
+    import sys
+
+    wl = WORKLOADS["1B"]
+    _, lay, sends = bench.ref_layout(wl, 1024)
+    cfg = bench.make_cfg(sd, wl, 1024)
+    assert sends[:40] == bench.calendar_sends(sd, cfg, 40)
+    for p, (blocks, emb) in enumerate(lay):
+        b, t_p, e = sd.sd_fragment_layout(cfg, p)
+        assert list(b) == blocks and bool(e) == emb
+    code = ("import sys, bench, argparse; bench.run_reference(argparse.Namespace(workload='toy', scale_block=1024, tau=None, "
+            "fragment_size=None, steps=1, warmup=1, gpus=1)); "
+            "import os; maps = open('/proc/self/maps').read(); "
+            "assert 'libsd.so' not in maps and 'paper_2501_18512_b200' not in sys.modules, 'libsd loaded'")
+    r = subprocess.run([sys.executable, "-c", code], cwd=bench.ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert '"impl": "reference"' in r.stdout
