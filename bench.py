@@ -656,7 +656,20 @@ def main():
             evs = calendar_sends(sd, cfg, base + 40)[base:]
             tl = args.timeline.replace(".json", f"_{kind}.json") if args.timeline else None
             overlap[kind] = overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, evs, dev,
-                                        kind=kind, timeline=tl)
+                                        kind=kind, timeline=tl,
+                                        gather_label=None if args.gather in ("push", "pull") else "copy engines")
+        if args.gather in ("auto", "ce") and world <= 32:
+            # the same check with the gather fused into the apply (pull): nothing is in flight during
+            # the inner steps; the transfer's cost moves into the apply (apply_after_window_ms)
+            psync = FragmentSync(cfg, n, rank, world, local, gather_mode=sd.SD_GATHER_PULL)
+            for i, kind in enumerate(("adamw", "gemm")):
+                base = 7 * (W + K) + 40 * i
+                evs = calendar_sends(sd, cfg, base + 40)[base:]
+                tl = args.timeline.replace(".json", f"_pull_{kind}.json") if args.timeline else None
+                overlap["pull_" + kind] = overlap_run(torch, dist, sd, synth, psync, cfg, theta, A, v, n, P, rank, world,
+                                                      evs, dev, kind=kind, timeline=tl, gather_label=None,
+                                                      ref=overlap[kind])
+            psync.close()
 
     extras = not args.no_extras and world == 1
     # ---- per-GPU kernel work at M = 1/2/4/8 replicas, emulated on this GPU (1 fragment)
@@ -842,7 +855,7 @@ def e2e_run(torch, dist, run, K, W, world, dev, offload):
 
 
 def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, world, events, dev, reps=15,
-                kind="adamw", timeline=None):
+                kind="adamw", timeline=None, gather_label="copy engines", ref=None):
     """SURVEY.md §8(d) hidden-gather check on the real NCCL path: per round,
     quantize -> all-gather on the comm stream while the compute stream runs
     tau synthetic inner steps -> block-receive -> apply.  exposed = window
@@ -882,7 +895,7 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
 
     comm = torch.cuda.ExternalStream(sync.ctx.sd_comm_stream(), device=dev)
     it = iter(events)
-    alone, gath, over, bytes_in, trace = [], [], [], [], None
+    alone, gath, over, bytes_in, app, trace = [], [], [], [], [], None
     for r in range(reps + 1):
         e = [Ev() for _ in range(6)]
         ti = [Ev() for _ in range(tau + 1)]      # inner-step boundaries of the overlapped window
@@ -927,13 +940,15 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
         alone.append(maxr_(e[0].elapsed_time(e[1])))
         gath.append(maxr_(e[2].elapsed_time(e[3])))
         over.append(maxr_(e[4].elapsed_time(e[5])))
+        app.append(maxr_(ap[0].elapsed_time(ap[1])))
         bytes_in.append((world - 1) * sync.payload[p])
         if timeline and r == reps // 2:
             z = q[0]
             us = lambda a, b: 1e3 * a.elapsed_time(b)  # noqa: E731
-            evs = [{"name": "k_quantize", "ph": "X", "pid": rank, "tid": "compute", "ts": 0.0, "dur": us(z, q[1])},
-                   {"name": f"all-gather (copy engines, {(world - 1) * sync.payload[p] / 1e6:.0f} MB in)", "ph": "X",
-                    "pid": rank, "tid": "comm", "ts": us(z, q[1]), "dur": us(q[1], gd)}]
+            evs = [{"name": "k_quantize", "ph": "X", "pid": rank, "tid": "compute", "ts": 0.0, "dur": us(z, q[1])}]
+            if gather_label:
+                evs.append({"name": f"all-gather ({gather_label}, {(world - 1) * sync.payload[p] / 1e6:.0f} MB in)",
+                            "ph": "X", "pid": rank, "tid": "comm", "ts": us(z, q[1]), "dur": us(q[1], gd)})
             for k in range(tau):
                 evs.append({"name": f"inner step {k + 1} ({kind})", "ph": "X", "pid": rank, "tid": "compute",
                             "ts": us(z, ti[k]), "dur": us(ti[k], ti[k + 1])})
@@ -958,6 +973,21 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
                            "otherData": {"what": f"one overlapped round, {world} ranks, tau = {tau}, inner = {kind}; "
                                                  "CUDA events on the compute and comm streams (ts relative to each "
                                                  "rank's quantize start)"}}, f)
+    if ref is not None:
+        # pull mode: no transfer is in flight during the inner steps -- the peers' payloads are read by the
+        # apply.  Judge the window against the copy-engine transfer of the same bytes (ref run), and report
+        # what the transfer costs inside the apply instead.
+        tg_ce = ref["gather_alone_ms"]
+        return {"tau": tau, "mode": "pull: the apply reads the peers' payloads over NVLink",
+                "inner_window_ms": ta, "overlap_window_ms": to, "exposed_ms": exposed,
+                "exposed_frac_of_gather": exposed / tg_ce if tg_ce > 0 else None,
+                "exposed_frac_of_window": exposed / ta if ta > 0 else None,
+                "hidden": exposed <= 0.05 * tg_ce,
+                "hidden_rule": "SURVEY.md §8(d): exposed <= 5% of the gather measured alone (the copy-engine "
+                               "transfer of the same payloads, from the copy-engine run)",
+                "wait_kernel_alone_ms": tg, "apply_after_window_ms": st.median(app),
+                "transfer_cost_in_apply_ms": st.median(app) - ref["apply_after_window_ms"],
+                "inner_slowdown": to / ta if ta > 0 else None, "reps": reps}
     return {"tau": tau, "inner_step": ("AdamW-shaped synthetic pass over the whole replica, 24 B/param (synth/)"
                                        if kind == "adamw" else "4 bf16 8192^3 cuBLAS matmuls (SM-bound)"),
             "inner_window_ms": ta, "overlap_window_ms": to, "gather_alone_ms": tg, "exposed_ms": exposed,
@@ -968,6 +998,7 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
             "gather_hbm_bytes_ms": hbm_ms,
             "exposed_within_gather_hbm_bytes": exposed <= hbm_ms,
             "inner_slowdown": to / ta if ta > 0 else None,
+            "apply_after_window_ms": st.median(app),
             "reps": reps,
             "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,
                        "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0}}

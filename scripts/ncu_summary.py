@@ -61,12 +61,13 @@ def emu_traffic(rep, traffic):
     return out
 
 
-rep = os.path.join(g, f"prof_{tag}.ncu-rep")
 traffic = {}
 tpath = os.path.join(out, "ncu_traffic.json")
 if os.path.exists(tpath):
     traffic = json.load(open(tpath))
-if os.path.exists(rep):
+
+
+def full_capture(rep, wl, title):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -76,7 +77,7 @@ if os.path.exists(rep):
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
             "launch__block_size", "smsp__inst_executed.sum", "lts__t_bytes.sum"]
     idx = {w: hdr.index(w) for w in want if w in hdr}
-    lines.append(f"\n## ncu --set full ({rep.split('/')[-1]})\n")
+    lines.append(f"\n## ncu --set full ({rep.split('/')[-1]}{title})\n")
     lines.append("| metric | " + " | ".join(r[idx['Kernel Name']].split('(')[0].replace('void ', '') for r in data) + " |")
     lines.append("|---|" + "---|" * len(data))
     for w in want[1:]:
@@ -87,8 +88,16 @@ if os.path.exists(rep):
         name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
         rd = float(r[idx["dram__bytes_read.sum"]].replace(",", "")) * scale.get(units[idx["dram__bytes_read.sum"]], 1)
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * scale.get(units[idx["dram__bytes_write.sum"]], 1)
-        traffic[f"{name}/{workload}"] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
-                                         "source": rep.split("/")[-1]}
+        traffic[f"{name}/{wl}"] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                                   "source": rep.split("/")[-1]}
+
+
+rep = os.path.join(g, f"prof_{tag}.ncu-rep")
+b0 = os.path.join(g, f"prof_b0_{tag}.ncu-rep")
+if os.path.exists(b0):
+    full_capture(b0, workload.replace("B1024", "B0"), ", B = 0: one scale per fragment, two passes")
+if os.path.exists(rep):
+    full_capture(rep, workload, "")
     emu = os.path.join(g, f"prof_emu_{tag}.ncu-rep")
     if os.path.exists(emu):
         rows = emu_traffic(emu, traffic)
