@@ -1124,13 +1124,40 @@ def b0_quantize_run(torch, sd, synth, wl, segs, n, dev, peak, reps=12):
         torch.cuda.synchronize()
         if r >= 2:
             ts.append(e0.elapsed_time(e1))
+    # the inner AdamW step before a send at B = 0: separate (AdamW, then both passes) vs fused
+    # (AdamW + block max in one pass, then the encode pass)
+    g = torch.randn(n, device=dev) * 1e-3
+    m1, m2 = torch.zeros(n, device=dev), torch.zeros(n, device=dev)
+    hp = sd.SdAdamW(lr=3e-4, beta1=0.9, beta2=0.99, eps=1e-8, weight_decay=0.1)
+    sep, fus = [], []
+    for r in range(reps + 2):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record()
+        ctx.sd_inner_adamw(r + 1, th, g, m1, m2, hp, n)
+        ctx.sd_outer_grad_quantize(0, t, th, A, slot, n)
+        e[1].record()
+        ctx.sd_fragment_sync(0, t, slot, n)
+        ctx.sd_merge(0, t + cfg.tau, slot, th, A, v, n)
+        e[2].record()
+        ctx.sd_inner_adamw_quantize(0, t, r + 1, th, g, m1, m2, A, slot, hp, n)
+        e[3].record()
+        ctx.sd_fragment_sync(0, t, slot, n)
+        ctx.sd_merge(0, t + cfg.tau, slot, th, A, v, n)
+        torch.cuda.synchronize()
+        if r >= 2:
+            sep.append(e[0].elapsed_time(e[1]))
+            fus.append(e[2].elapsed_time(e[3]))
     ctx.sd_finalize()
     tq = statistics.median(ts)
+    ts_, tf_ = statistics.median(sep), statistics.median(fus)
     alg, moved = 8.5 * n + 4, 16.5 * n + 4
     return {"fragment_elems": int(n), "quantize_ms": tq, "kernels": "k_absmax + k_encode (two passes)",
             "frac_algorithmic": alg / (tq / 1e3) / 1e9 / peak, "frac_moved": moved / (tq / 1e3) / 1e9 / peak,
             "algorithmic_bytes_per_elem": 8.5, "moved_bytes_per_elem": 16.5,
-            "achieved_over_algorithmic_bytes": moved / alg}
+            "achieved_over_algorithmic_bytes": moved / alg,
+            "inner_adamw_before_send": {"separate_ms": ts_, "fused_ms": tf_, "speedup": ts_ / tf_,
+                                        "moved_bytes_per_elem": {"separate": 28 + 16.5, "fused": 32 + 8.5},
+                                        "fused_frac_moved": (40.5 * n) / (tf_ / 1e3) / 1e9 / peak}}
 
 
 def m_sweep_run(torch, sd, synth, cfg, segs, n, B, dev, peak, iters=12):

@@ -395,6 +395,8 @@ __device__ __forceinline__ void absmax_chunk(const QArgs& a, int64_t c, int lane
   run = max(run, m);
 }
 
+__device__ __forceinline__ void flush_block_max(const QArgs& a, int lane, int64_t cur, uint32_t run);
+
 __global__ void __launch_bounds__(kThreads) k_absmax(QArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -404,8 +406,12 @@ __global__ void __launch_bounds__(kThreads) k_absmax(QArgs a) {
   uint32_t run = 0;
   for (int64_t c = warp; c < nfull; c += nwarps) absmax_chunk<true>(a, c, lane, cur, run);
   if ((nfull << 10) < a.n && warp == nfull % nwarps) absmax_chunk<false>(a, nfull, lane, cur, run);
-  // merge the CTA's warps that ended in the same block: one atomic per distinct
-  // block per CTA (B = 0: one per CTA instead of one per warp)
+  flush_block_max(a, lane, cur, run);
+}
+
+// Merges the CTA's warps that ended in the same block: one atomic per distinct
+// block per CTA (B = 0: one per CTA instead of one per warp).
+__device__ __forceinline__ void flush_block_max(const QArgs& a, int lane, int64_t cur, uint32_t run) {
   __shared__ int64_t s_blk[kThreads / 32];
   __shared__ uint32_t s_run[kThreads / 32];
   if (lane == 0) {
@@ -674,8 +680,10 @@ __device__ __forceinline__ void adamw_chunk(const QArgs& a, const AdamArgs& h, i
   }
 }
 
+// 3 CTAs/SM (<= 85 registers; ptxas spills ~50 B): 0.770 vs 0.792 ms per 1B fragment at
+// 2 CTAs/SM and 124 registers (profiles/r2_kernel_ab.txt)
 template <int NB>
-__global__ void __launch_bounds__(kThreads) k_adamw_quantize(QArgs a, AdamArgs h) {
+__global__ void __launch_bounds__(kThreads, 3) k_adamw_quantize(QArgs a, AdamArgs h) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -692,6 +700,81 @@ __global__ void __launch_bounds__(kThreads) k_adamw_quantize(QArgs a, AdamArgs h
   }
   if (blockIdx.x == 0) write_tail(a);
   if (a.sig) signal_round(a);
+}
+
+// AdamW on a chunk fused with the first pass of the two-pass quantize (B = 0,
+// SPEC.md:266, or B > 1024): the updated theta is written and its Delta's
+// block max accumulated in the same pass, so the inner step before a send
+// costs 32 + 8.5 B/param (k_encode re-reads theta and A) instead of
+// 28 + 16.5 with a separate absmax pass.
+template <bool kFullChunk>
+__device__ __forceinline__ void adamw_absmax_chunk(const QArgs& a, const AdamArgs& h, int64_t c, int lane,
+                                                   int64_t& cur, uint32_t& run) {
+  // row by row (no Delta kept past its row): the block max and the first
+  // non-finite index only need a running max and a running min
+  const int64_t e0 = c * 1024 + 8 * lane;
+  uint32_t mx = 0, bad = 0xffffffffu;
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k) {
+    const int64_t e = e0 + 256 * k;
+    float d[8];
+    if (kFullChunk) {
+      f8 t = ld8(h.theta + e), g = ld8_stream(h.grad + e), m = ld8(h.m + e), v = ld8(h.v + e);
+      const f8 an = ld8_stream(a.anchor + e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        adamw_one(t.v[j], g.v[j], m.v[j], v.v[j], h);
+        d[j] = __fsub_rn(an.v[j], t.v[j]);  // Alg. 2 L7 on the updated theta
+      }
+      st8(h.theta + e, t);
+      st8(h.m + e, m);
+      st8(h.v + e, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        d[j] = 0.0f;
+        if (e + j < a.n) {
+          float t = h.theta[e + j], m = h.m[e + j], v = h.v[e + j];
+          adamw_one(t, h.grad[e + j], m, v, h);
+          h.theta[e + j] = t;
+          h.m[e + j] = m;
+          h.v[e + j] = v;
+          d[j] = __fsub_rn(a.anchor[e + j], t);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // rows ascending, then j ascending: the lane's first bad index
+      const uint32_t ab = abs_bits(d[j]);
+      mx = max(mx, ab);
+      if (ab >= kInfBits && bad == 0xffffffffu) bad = (uint32_t)(256 * k + 8 * lane + j);
+    }
+  }
+  const uint32_t m = __reduce_max_sync(kFull, mx);
+  if (m >= kInfBits) {  // index of the first non-finite Delta of the chunk (as record_first_bad)
+    const uint32_t b = __reduce_min_sync(kFull, bad);
+    if (lane == 0 && b != 0xffffffffu)
+      atomicMin(reinterpret_cast<unsigned long long*>(a.slot + a.trailer_off + 8), (unsigned long long)(c * 1024 + b));
+  }
+  const int64_t blk = block_of_chunk(a, c);
+  if (blk != cur) {
+    if (cur >= 0 && lane == 0) atomicMax(reinterpret_cast<unsigned int*>(a.slot + a.scales_off) + cur, run);
+    cur = blk;
+    run = 0;
+  }
+  run = max(run, m);
+}
+
+__global__ void __launch_bounds__(kThreads, 3) k_adamw_absmax(QArgs a, AdamArgs h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nfull = a.n >> 10;
+  int64_t cur = -1;
+  uint32_t run = 0;
+  for (int64_t c = warp; c < nfull; c += nwarps) adamw_absmax_chunk<true>(a, h, c, lane, cur, run);
+  if ((nfull << 10) < a.n && warp == nfull % nwarps) adamw_absmax_chunk<false>(a, h, nfull, lane, cur, run);
+  flush_block_max(a, lane, cur, run);
 }
 
 // ---------------------------------------------------------------------------
@@ -984,6 +1067,36 @@ int maybe_signal(const Round& rd, const QArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+namespace {
+// Two passes (B = 0 or B > 1024): the scales come from atomics, so the slot
+// is built locally; in push mode the finished slot is then pushed (and the
+// round signalled) by k_push_copy.  Pass 1 is k_absmax, or k_adamw_absmax
+// when an AdamW step is fused in (h != nullptr).
+int two_pass(const QArgs& a, const Round& rd, const Payload& pl, uint8_t* slot, int num_sms, cudaStream_t st,
+             const AdamArgs* h) {
+  const int64_t chunks = (pl.n + 1023) >> 10;
+  const int wpb = kThreads / 32;
+  QArgs loc = a;
+  loc.push = 0;
+  loc.sig = a.sig && !a.push;
+  if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
+  QArgs pass1 = loc;
+  pass1.sig = 0;
+  if (h)
+    k_adamw_absmax<<<grid_for(k_adamw_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1, *h);
+  else
+    k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1);
+  k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
+  int launched = 2;
+  if (a.push) {
+    k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
+    launched = 3;
+  }
+  launched += maybe_signal(rd, a, st);
+  return cudaGetLastError() == cudaSuccess ? launched : -1;
+}
+}  // namespace
+
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Round& rd,
                     int num_sms, cudaStream_t st) {
   const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
@@ -997,23 +1110,7 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
     const int ks = maybe_signal(rd, a, st);
     return cudaGetLastError() == cudaSuccess ? 1 + ks : -1;
   }
-  // two passes: the scales come from atomics, so the slot is built locally;
-  // in push mode the finished slot is then pushed (and the round signalled) by k_push_copy
-  QArgs loc = a;
-  loc.push = 0;
-  loc.sig = a.sig && !a.push;
-  if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
-  QArgs pass1 = loc;
-  pass1.sig = 0;
-  k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1);
-  k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
-  int launched = 2;
-  if (a.push) {
-    k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
-    launched = 3;
-  }
-  launched += maybe_signal(rd, a, st);
-  return cudaGetLastError() == cudaSuccess ? launched : -1;
+  return two_pass(a, rd, pl, slot, num_sms, st, nullptr);
 }
 
 int launch_round_wait(const RoundRecv& rr, const Payload& pl, int M, uint64_t timeout_ns, unsigned long long* status,
@@ -1068,14 +1165,9 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
                           uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st) {
-  if (!single_pass(pl.B)) {  // two-pass scales: AdamW, then quantize
-    const int k1 = launch_adamw(theta, grad, m, v, pl.n, hp, num_sms, st);
-    if (k1 < 0) return -1;
-    const int k2 = launch_quantize(theta, anchor, pl, slot, rd, num_sms, st);
-    return k2 < 0 ? -1 : k1 + k2;
-  }
   const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
   const AdamArgs h = make_adam(theta, grad, m, v, pl.n, hp);
+  if (!single_pass(pl.B)) return two_pass(a, rd, pl, slot, num_sms, st, &h);  // AdamW + block max, then encode
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int g = grid_for(k_adamw_quantize<1>, num_sms, chunks > 0 ? chunks : 1, kThreads / 32);
   if (pl.B == 1024)

@@ -76,7 +76,8 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
                  cudaStream_t st);
 
 // AdamW step fused with Delta + E3M0 of the updated theta into one payload
-// (single pass for B in {256, 512, 1024}; AdamW + two-pass quantize otherwise).
+// (single pass for B in {256, 512, 1024}; otherwise AdamW fused with the first
+// pass -- the block max -- then k_encode).
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
                           uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st);
 

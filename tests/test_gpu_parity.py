@@ -543,6 +543,38 @@ def test_inner_adamw_quantize_fused_bit_exact(n, B):
     rep.close()
 
 
+@pytest.mark.parametrize("B", [1024, 0, 4096])
+def test_inner_adamw_quantize_fused_poison_index(B):
+    """Non-finite updated parameters in the fused AdamW + quantize (single pass,
+    and for B = 0 / 4096 the AdamW + block-max first pass): the payload records
+    the first non-finite Delta's index exactly as or_quantize does."""
+    rng = np.random.default_rng(B + 5)
+    n = 3 * 4096 + 77
+    A = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    th = (A - rng.standard_normal(n).astype(np.float32) * 1e-3).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    th[n - 3] = np.nan
+    th[9000] = np.inf
+    th[5000] = -np.inf
+    g[7001] = np.nan
+    cfg = cfg_for(B)
+    rep = EmulatedReplicas(cfg, 1, n)
+    hp = sd.SdAdamW(**HP)
+    th_d = to_dev(th)
+    rep.ctx[0].sd_inner_adamw_quantize(0, 10, 3, th_d, to_dev(g), to_dev(m), to_dev(v), to_dev(A), rep.slot(0), hp, n)
+    torch.cuda.synchronize()
+    oracle.adamw(th, g, m, v, 3, lr=HP["lr"], b1=HP["beta1"], b2=HP["beta2"], eps=HP["eps"], wd=HP["weight_decay"])
+    want, poisoned = oracle.quantize(th, A, B)
+    assert poisoned
+    got = rep.gather.cpu().numpy()
+    assert oracle.payload_poisoned(got, n, B) == oracle.payload_poisoned(want, n, B) == (1, 5000)
+    assert np.array_equal(th_d.cpu().numpy(), th, equal_nan=True)  # NaN payload bits may differ (CPU vs GPU)
+    rep.ctx[0].sd_fragment_sync(0, 10, rep.gather, n)
+    rep.close()
+
+
 @pytest.mark.parametrize("B", [0, 256, 1024, 4096])
 @pytest.mark.parametrize("n", [1, 9, 1023, 4099, 65536 + 13])
 def test_no_writes_outside_buffers(n, B):
