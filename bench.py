@@ -282,7 +282,8 @@ def _oracle_rate(wl, B, M, order, segs, n, target_s):
             break
     _SAMPLES.clear()
     return total_e * M / total_t, f"or_round on {', '.join(used)} (calendar order), all M={M} replicas: " \
-                                  f"{total_e} elements in {total_t:.2f} s"
+                                  f"{total_e} elements in {total_t:.2f} s (n / t = {total_e / total_t:.4g} fragment " \
+                                  f"elements per second; value = M n / t, work-normalized)"
 
 
 def cpu_baseline(wl, B, M, order, segs, n, target_s):
@@ -574,7 +575,9 @@ def main():
         events = more_ev
         remeasured = True
     ms_eager = None
-    use_graph = args.graph == "on" or (args.graph == "auto" and flush and world == 1)
+    # graphs: small L2-resident configs on one GPU (with N > 1, capturing the step with NCCL's all-gather
+    # in it hung on B200 -- not used; the fused modes' round ids are host counters baked into the kernels)
+    use_graph = (args.graph == "on" and world == 1) or (args.graph == "auto" and flush and world == 1)
     if use_graph:
         # Launch-bound small fragments: capture one serialized step per fragment of a
         # calendar cycle as a CUDA graph (libsd's calls are stream-ordered and
@@ -1001,7 +1004,11 @@ def overlap_run(torch, dist, sd, synth, sync, cfg, theta, A, v, n, P, rank, worl
             "apply_after_window_ms": st.median(app),
             "reps": reps,
             "nvlink": {"ingress_bytes_per_gpu": int(st.median(bytes_in)), "GBps_per_direction": gbps,
-                       "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0}}
+                       "frac_of_900_nominal": gbps / 900.0, "frac_of_770_measured_peer": gbps / 770.0,
+                       "projection_M8_gather_ms": (7 * st.median(bytes_in) / max(1, world - 1)) / (gbps * 1e6)
+                       if world < 8 else None,
+                       "projection_note": "PROJECTION (not measured): 7 payloads of this size at the ingress rate "
+                                          "measured here; gpurun offers at most 4 GPUs"}}
 
 
 def fused_inner_run(torch, sd, sync, cfg, th, A0, n, B, dev, peak, reps=8):

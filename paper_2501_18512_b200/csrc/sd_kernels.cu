@@ -10,6 +10,12 @@
 //               Nesterov, anchor update, alpha-merge.
 //   k_absmax + k_encode: the two-pass variant for B = 0 (one scale per
 //               fragment) and B > 1024.
+// Around them: the fused all-gather protocol (push: NVLink stores from the
+// quantize; pull: NVLink loads in the apply; round flags signalled by the
+// payload kernel's last CTA or a one-thread kernel, k_round_wait for the
+// block-receive) and the AdamW inner step fused with
+// the quantize or its first pass (k_adamw_quantize, k_adamw_absmax) and with
+// the apply (k_apply<M, true>) -- SURVEY.md §8(f) NEXT-1/NEXT-2.
 //
 // Memory: every lane moves 8 consecutive fp32 with one 256-bit access
 // (sm_100 LDG.256 / STG.256), so a warp instruction covers 1 KB and a lane's
