@@ -28,7 +28,8 @@
  *    sd_gather_alloc in NCCL symmetric memory, which lets the all-gather run
  *    on the copy engines with zero SMs.  Apart from those and NCCL
  *    internals the library allocates no device memory, and it writes only
- *    slot_out, gather_buf, anchor, momentum and theta.
+ *    slot_out, gather_buf, anchor, momentum, theta and the caller's
+ *    quantize workspace (sd_set_workspace).
  *  - sd_stream is a cudaStream_t (NULL = legacy default stream).  Every
  *    device call is stream-ordered and asynchronous; errors raised on the
  *    device (non-finite outer gradients, NCCL async errors) surface at
@@ -263,6 +264,27 @@ sd_status sd_inner_adamw(sd_ctx* ctx, int64_t k, float* theta, const float* grad
 sd_status sd_inner_adamw_quantize(sd_ctx* ctx, int32_t p, int64_t t, int64_t k, float* theta, const float* grad,
                                   float* m, float* v, const float* anchor, int64_t n, void* slot_out,
                                   const sd_adamw* hp, sd_stream stream);
+
+/* Scratch of the two-pass quantize.  With B = 0 (one scale per fragment,
+ * S:266) or B >= 2048 every code depends on a block maximum over more data
+ * than one pass keeps on chip, so the quantize makes two passes (block max,
+ * then encode).  Without a workspace the second pass re-reads theta and A
+ * (16.5 B/param moved for 8.5 needed).  With one, the first pass also writes
+ * a 16-bit summary of every Delta there and the second pass encodes from it,
+ * re-reading theta and A only for the rare elements whose summary straddles
+ * a code threshold (about 1 in 4000) -- same codes, bit for bit.
+ *  sd_quantize_workspace_bytes: bytes needed for a fragment of n elements
+ *    (0 when the single pass applies: B in {256, 512, 1024}, or n == 0, or an
+ *    invalid cfg).
+ *  sd_set_workspace: caller-owned device memory, 256-byte aligned (NULL or 0
+ *    bytes detaches).  Used by sd_outer_grad_quantize and
+ *    sd_inner_adamw_quantize for every fragment whose need fits in `bytes`
+ *    (others take the re-reading pass).  Its contents between calls are
+ *    meaningless; the calls that use it must be ordered with each other (one
+ *    stream, as Alg. 2's sends are), and it must stay alive until that
+ *    stream's work using it is done. */
+size_t sd_quantize_workspace_bytes(const sd_config* cfg, int64_t n);
+sd_status sd_set_workspace(sd_ctx* ctx, void* ws, size_t bytes);
 
 /* Alg. 2 L7 + E3M0 (§8(a) a3).  p must be scheduled to send at t and not be
  * in flight.  Reads theta[n], anchor[n]; writes one payload

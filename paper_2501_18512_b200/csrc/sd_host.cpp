@@ -173,6 +173,7 @@ struct sd_ctx {
   };
   std::vector<Drain> drains;
   std::vector<Inflight> fl;
+  sdk::Workspace ws;                          // caller-owned scratch of the two-pass quantize (sd_set_workspace)
   unsigned long long* status_host = nullptr;  // {first_bad, code, dead}: pinned, mapped
   unsigned long long* status_dev = nullptr;
   char err[512] = "";
@@ -721,6 +722,26 @@ sd_status adam_hyper(sd_ctx* c, int64_t k, const sd_adamw* hp, sdk::AdamHyper* h
 
 }  // namespace
 
+size_t sd_quantize_workspace_bytes(const sd_config* cfg, int64_t n) {
+  if (!cfg || validate(cfg, nullptr, 0) != SD_OK || n <= 0) return 0;
+  const int32_t B = cfg->scale_block;
+  if (B == 256 || B == 512 || B == 1024) return 0;  // single pass: no scratch
+  return sdk::stage_bytes(n);
+}
+
+sd_status sd_set_workspace(sd_ctx* c, void* ws, size_t bytes) {
+  if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
+  if (ws == nullptr || bytes == 0) {
+    c->ws = sdk::Workspace();
+    return SD_OK;
+  }
+  sd_status st;
+  if ((st = check_ptr(c, ws, 256, "workspace"))) return st;
+  c->ws.ptr = static_cast<uint8_t*>(ws);
+  c->ws.bytes = bytes;
+  return SD_OK;
+}
+
 sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* theta, const float* anchor,
                                  int64_t n, void* slot_out, sd_stream stream) {
   if (!c) return fail(g_err, SD_ERR_ARG, "ctx is NULL");
@@ -729,7 +750,8 @@ sd_status sd_outer_grad_quantize(sd_ctx* c, int32_t p, int64_t t, const float* t
   PushRound pr;
   sd_status st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
-  const int k = sdk::launch_quantize(theta, anchor, pl, local_slot(c, slot_out, pr, pl), pr.round, c->num_sms, s);
+  const int k =
+      sdk::launch_quantize(theta, anchor, pl, local_slot(c, slot_out, pr, pl), pr.round, c->num_sms, s, c->ws);
   if (k < 0) return cuda_fail(c, cudaGetLastError(), "k_quantize launch");
   g_launches += (uint64_t)k;
   return end_send(c, p, t, n, slot_out, pr);
@@ -769,7 +791,7 @@ sd_status sd_inner_adamw_quantize(sd_ctx* c, int32_t p, int64_t t, int64_t k, fl
   st = begin_send(c, p, t, theta, anchor, n, slot_out, s, &pl, &pr);
   if (st != SD_OK) return st;
   const int kl = sdk::launch_adamw_quantize(theta, grad, m, v, anchor, pl, local_slot(c, slot_out, pr, pl), h,
-                                            pr.round, c->num_sms, s);
+                                            pr.round, c->num_sms, s, c->ws);
   if (kl < 0) return cuda_fail(c, cudaGetLastError(), "k_adamw_quantize launch");
   g_launches += (uint64_t)kl;
   return end_send(c, p, t, n, slot_out, pr);

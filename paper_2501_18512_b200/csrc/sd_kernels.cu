@@ -62,6 +62,15 @@ __device__ __forceinline__ f8 ld8_stream(const float* p) {
                : "l"(p));
   return r;
 }
+// the same, evict-first in L2 (data this pass reads once and nobody re-reads soon)
+__device__ __forceinline__ f8 ld8_stream_ef(const float* p) {
+  f8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                 "=f"(r.v[6]), "=f"(r.v[7])
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ f8 ld8(const float* p) {
   f8 r;
   asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -69,6 +78,9 @@ __device__ __forceinline__ f8 ld8(const float* p) {
                  "=f"(r.v[6]), "=f"(r.v[7])
                : "l"(p));
   return r;
+}
+__device__ __forceinline__ void st_global_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st8(float* p, const f8& r) {
   asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
@@ -150,6 +162,14 @@ struct QArgs {
   size_t flags_off;
   unsigned long long seq;
   unsigned int* counter;
+  // staged two-pass quantize (B = 0 or B > 1024, caller workspace): pass 1
+  // also writes a 16-bit summary of every Delta (2 per word; chunk c, row k,
+  // lane l at word c*512 + 128k + 4l) and each row's max |Delta| bits
+  // (stg_max[4c + k]); pass 2 encodes from them.  Null: pass 2 re-reads theta, A.
+  uint32_t* stg;
+  uint32_t* stg_max;
+  int stg_hints;    // bit 0: pass 1 reads theta, A (and g) L2 evict-first; bit 1: pass 2 discards consumed lines
+  int64_t stg_keep_from;  // pass 1 stores the summaries of chunks >= this L2 evict-last (pass 2 reads them first)
 };
 
 __device__ __forceinline__ void push_u32(const QArgs& a, size_t off, uint32_t v) {
@@ -195,15 +215,15 @@ __device__ __forceinline__ void signal_round(const QArgs& a) {
 // Chunk = 1024 elements = 4 rows of 256; lane `lane` owns elements
 // c*1024 + k*256 + 8*lane .. +7 of row k (one LDG.256 per array and row).
 // Elements past n of the ragged last chunk read as Delta = +0.
-template <bool kFullChunk>
+template <bool kFullChunk, bool kEvictFirst = false>
 __device__ __forceinline__ void load_chunk(const QArgs& a, int64_t c, int lane, f8 (&d)[4]) {
   const int64_t e0 = c * 1024 + 8 * lane;
   if (kFullChunk) {
     f8 th[4], an[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      th[k] = ld8_stream(a.theta + e0 + 256 * k);
-      an[k] = ld8_stream(a.anchor + e0 + 256 * k);
+      th[k] = kEvictFirst ? ld8_stream_ef(a.theta + e0 + 256 * k) : ld8_stream(a.theta + e0 + 256 * k);
+      an[k] = kEvictFirst ? ld8_stream_ef(a.anchor + e0 + 256 * k) : ld8_stream(a.anchor + e0 + 256 * k);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -383,14 +403,65 @@ __device__ __forceinline__ int64_t block_of_chunk(const QArgs& a, int64_t c) {
   return a.lgB < 0 ? 0 : ((c << 10) >> a.lgB);
 }
 
-template <bool kFullChunk>
+// Staged two-pass: pass 1 keeps, per element, a 16-bit
+// summary of |Delta| relative to its row's max m_r (256 elements):
+//   base = bits(2^(exp(m_r) - 7)) (0 if that is subnormal),
+//   o = clamp(bits|Delta| - base, 0, 2^26 - 1), summary = (o >> 11) | sign << 15,
+// i.e. |Delta|'s bit pattern to within a bucket of 2^11 ulps (12 mantissa
+// bits) over the 8 octaves below m_r.  Any scale s >= m_r puts T_6(s) >=
+// m_r 2^-6.5 above the bucket of everything below base, so those code 0.
+// Pass 2 evaluates the (monotone) fast-path code at both ends of the bucket;
+// if they agree that is the code, else (about 1 element in 4000) it re-reads
+// theta and A for that element and encodes it exactly.
+__device__ __forceinline__ uint32_t stage_base(uint32_t mbits) {
+  const uint32_t E = mbits & kInfBits;
+  return E >= (7u << 23) ? E - (7u << 23) : 0u;
+}
+__device__ __forceinline__ uint32_t stage16(float d, uint32_t base) {
+  const uint32_t b = abs_bits(d);
+  const uint32_t o = b > base ? min(b - base, 0x3ffffffu) : 0u;
+  return (o >> 11) | ((__float_as_uint(d) >> 16) & 0x8000u);
+}
+__device__ __forceinline__ void stage_row(const QArgs& a, int64_t c, int k, int lane, const float* d, uint32_t mbits) {
+  const uint32_t base = stage_base(mbits);
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = stage16(d[2 * i], base) | (stage16(d[2 * i + 1], base) << 16);
+  if (c >= a.stg_keep_from) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a.stg + c * 512 + 128 * k + 4 * lane),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(a.stg + c * 512 + 128 * k + 4 * lane), "r"(w[0]),
+                 "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+}
+
+template <bool kFullChunk, bool kStage, bool kEF>
 __device__ __forceinline__ void absmax_chunk(const QArgs& a, int64_t c, int lane, int64_t& cur, uint32_t& run) {
   f8 d[4];
-  load_chunk<kFullChunk>(a, c, lane, d);
+  load_chunk<kFullChunk, kEF>(a, c, lane, d);
   uint32_t m = 0;
+  if (kStage) {
+    uint32_t mr[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) m = max(m, row_max_bits(d[k]));
-  m = __reduce_max_sync(kFull, m);
+    for (int k = 0; k < 4; ++k) {
+      mr[k] = __reduce_max_sync(kFull, row_max_bits(d[k]));
+      m = max(m, mr[k]);
+      stage_row(a, c, k, lane, d[k].v, mr[k]);
+    }
+    if (lane == 0)
+      asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(a.stg_max + 4 * c), "r"(mr[0]), "r"(mr[1]),
+                   "r"(mr[2]), "r"(mr[3])
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m = max(m, row_max_bits(d[k]));
+    m = __reduce_max_sync(kFull, m);
+  }
   if (m >= kInfBits) record_first_bad(a, c, lane, d);
   const int64_t blk = block_of_chunk(a, c);
   if (blk != cur) {
@@ -403,15 +474,17 @@ __device__ __forceinline__ void absmax_chunk(const QArgs& a, int64_t c, int lane
 
 __device__ __forceinline__ void flush_block_max(const QArgs& a, int lane, int64_t cur, uint32_t run);
 
-__global__ void __launch_bounds__(kThreads) k_absmax(QArgs a) {
+// staged: 3 CTAs/SM (<= 85 registers) as k_quantize
+template <bool kStage, bool kEF>
+__global__ void __launch_bounds__(kThreads, kStage ? 3 : 1) k_absmax(QArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nfull = a.n >> 10;
   int64_t cur = -1;
   uint32_t run = 0;
-  for (int64_t c = warp; c < nfull; c += nwarps) absmax_chunk<true>(a, c, lane, cur, run);
-  if ((nfull << 10) < a.n && warp == nfull % nwarps) absmax_chunk<false>(a, nfull, lane, cur, run);
+  for (int64_t c = warp; c < nfull; c += nwarps) absmax_chunk<true, kStage, kEF>(a, c, lane, cur, run);
+  if ((nfull << 10) < a.n && warp == nfull % nwarps) absmax_chunk<false, kStage, kEF>(a, nfull, lane, cur, run);
   flush_block_max(a, lane, cur, run);
 }
 
@@ -449,19 +522,243 @@ __device__ __forceinline__ void encode_chunk(const QArgs& a, int64_t c, int lane
   encode_chunk_rows<1, kFullChunk>(a, c, lane, d, s);
 }
 
+// Pass 2 from the staged summaries (fast path only: the block's thresholds
+// T_j = T_0 / 2^j are normal; zero and non-finite scales give all-zero codes,
+// as e3m0_threshold's +inf thresholds do).  In bucket units of a row
+// (u = (bits|Delta| - base) / 2^11, summary u = floor of it): a_0 = bits(T_0)
+// - base = 2^11 q_0 + r_0 and a_j = a_0 - j 2^23, so the bucket lies at or
+// above T_j iff u >= q_0 + (r_0 != 0) - 4096 j, i.e. with
+// D = q_0 + (r_0 != 0) + 4095 and K = 32767 - D the code magnitude is
+//   e = max(floor((u + K) / 4096), 0)      (<= 7: u <= D since |Delta| <= s < 2 T_0),
+// and the bucket straddles a threshold iff r_0 != 0 and u == q_0 (mod 4096)
+// -- those elements re-read theta and A and encode exactly.  Everything
+// below base was stored as u = 0, whose e is 0 (a_0 >= 6.41 octaves).
+// SIMD form per 32-bit word (two summaries): v = (word & 0x7fff7fff) +
+// (K + 2^15) per half (K clamped to >= -2^15, so each half stays in
+// [0, 2^16): no carry between halves); the high nibble of each half is
+// n = e_raw + 8, i.e. e > 0 iff n >= 9, and then the code is (n & 7) | sign << 3.
+// Straddling (r_0 != 0): u - q_0 == 0 (mod 4096) iff the low 12 bits of the
+// half of v are all ones (q_0 + K + 2^15 == -1 mod 4096), i.e. iff adding 1
+// carries into bit 12.  The 8 high nibbles and 8 sign bits of a lane's row
+// are gathered with PRMT into the row's code word (nibble i = element i).
+__device__ __forceinline__ uint32_t gather_hi_nibbles(const uint32_t (&v)[4]) {
+  const uint32_t A = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);  // bytes 1
+  const uint32_t B = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);  // bytes 3
+  return ((A >> 4) & 0x0f0f0f0fu) | (B & 0xf0f0f0f0u);  // nibble 2k: low half of word k, 2k+1: high half
+}
+
+// The code word of one row of one lane; *straddle = some element needs the exact re-read.
+__device__ __forceinline__ uint32_t staged_row_codes(uint32_t t0bits, uint32_t row_max, const uint4& qv,
+                                                     bool* straddle) {
+  const uint32_t a0 = t0bits - stage_base(row_max);
+  const uint32_t rho = (a0 & 2047u) != 0u ? 1u : 0u;
+  const int K = max(32767 - (int)((a0 >> 11) + rho + 4095u), -32768);
+  const uint32_t Kpair = (uint32_t)(K + 32768) * 0x10001u;
+  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+  uint32_t v[4], acc = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = (qw[i] & 0x7fff7fffu) + Kpair;
+    acc |= v[i] ^ (v[i] + 0x00010001u);  // bit 12 / 28 flips iff the half's low 12 bits are all ones
+  }
+  *straddle = rho && (acc & 0x10001000u);
+  const uint32_t n = gather_hi_nibbles(v);
+  const uint32_t sg = gather_hi_nibbles(qw) & 0x88888888u;                        // sign -> bit 3 of each nibble
+  const uint32_t keep3 = ((n & 0x77777777u) + 0x77777777u) & n & 0x88888888u;  // bit 3 set iff n >= 9
+  const uint32_t M = keep3 | (keep3 - (keep3 >> 3));                          // 0xF per kept nibble
+  return (n ^ sg ^ 0x88888888u) & M;                                            // (n & 7) | sign << 3
+}
+
+// Exact codes for the straddling elements of a row (rare).
+__device__ __forceinline__ uint32_t staged_row_fixup(const float* __restrict__ theta, const float* __restrict__ anchor,
+                                                  int64_t n, int64_t e0, uint32_t t0bits, uint32_t row_max, uint4 qv,
+                                                  uint32_t w) {
+  const uint32_t a0 = t0bits - stage_base(row_max);
+  const uint32_t q0 = a0 >> 11;
+  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t u = (qw[i >> 1] >> (16 * (i & 1))) & 0x7fffu;
+    if (((u ^ q0) & 0xfffu) != 0u) continue;
+    const int64_t idx = e0 + i;
+    const uint32_t code = idx < n ? encode_fast(__fsub_rn(anchor[idx], theta[idx]), t0bits + 0x7fffffu) : 0u;
+    w = (w & ~(0xfu << (4 * i))) | (code << (4 * i));
+  }
+  return w;
+}
+
+// Pass 2 without a workspace: re-reads theta and A (k_encode), last chunk
+// first (pass 1 streamed the fragment forward, so its tail is what the L2
+// still holds).
 __global__ void __launch_bounds__(kThreads, 3) k_encode(QArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nfull = a.n >> 10;
   const int64_t nchunks = nfull + ((nfull << 10) < a.n ? 1 : 0);
-  // last chunk first: k_absmax streamed the fragment forward, so its tail is
-  // what the L2 still holds when this second pass starts
   for (int64_t k = warp; k < nchunks; k += nwarps) {
     const int64_t c = nchunks - 1 - k;
     if (c < nfull) encode_chunk<true>(a, c, lane);
     else encode_chunk<false>(a, c, lane);
   }
+  if (blockIdx.x == 0) write_tail(a);
+  if (a.sig) signal_round(a);
+}
+
+// T_0(s) = smallest binary32 c with c^2 >= s^2 / 2 (e3m0_threshold(s, 0)),
+// for a normal s >= 2^-100 (the fast path's range): fl(s * fl(1/sqrt 2)) is
+// within 2 ulps of it, then exact binary64 checks step to it.  Inline, so
+// every lane of a warp computes it without a call or a shuffle.
+__device__ __forceinline__ float e3m0_t0_normal(float s) {
+  const double b = __dmul_rn(__dmul_rn((double)s, (double)s), 0.5);  // exact
+  float c = __fmul_rn(s, 0.70710678f);
+#pragma unroll 1
+  while (__dmul_rn((double)c, (double)c) < b) c = __uint_as_float(__float_as_uint(c) + 1u);
+#pragma unroll 1
+  for (;;) {
+    const float pc = __uint_as_float(__float_as_uint(c) - 1u);
+    if (__dmul_rn((double)pc, (double)pc) >= b) c = pc; else break;
+  }
+  return c;
+}
+
+// Pass 2 from the summaries (k_encode_staged): one CTA per tile of
+// 8 kStagedCpw chunks, tiles walked last to first (pass 1 streamed the
+// fragment forward, so its tail is what the L2 still holds).  Each warp
+// issues the loads of all its chunks' summaries (2 KB + 16 B each) before it
+// encodes any, and the code is kept small (the straddle fix-up and the
+// re-reading fallback are off the straight path): a persistent 2-CTA/SM form with a 3-deep
+// software pipeline ran at 1.8 TB/s, stalled on instruction fetch
+// (profiles/r2_b0_staged.txt).  Codes are stored locally (the two-pass paths
+// push the finished slot separately).
+__device__ __forceinline__ void encode_chunk_call(const QArgs& a, int64_t c, int lane, bool full) {
+  if (full) encode_chunk<true>(a, c, lane);
+  else encode_chunk<false>(a, c, lane);
+}
+
+struct Staged {
+  uint4 mr;
+  uint4 q[4];
+};
+
+__device__ __forceinline__ void load_staged(const QArgs& a, int64_t c, int lane, Staged& st) {
+  st.mr = __ldg(reinterpret_cast<const uint4*>(a.stg_max + 4 * c));
+  const uint4* p = reinterpret_cast<const uint4*>(a.stg + c * 512 + 4 * lane);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) st.q[k] = __ldg(p + 32 * k);
+}
+
+// The fast path of one chunk (s, t0b: its block scale and bits(T_0(s)), t0b
+// = 0 off the fast path).  Stores the codes read off the summaries and
+// returns the work left for after the chunk loop, so that nothing is live
+// across it: bit k = row k of this lane straddles a threshold (re-encode it
+// exactly), bit 4 = the block's thresholds are below the normal range
+// (re-read the chunk, explicit compares).
+__device__ __forceinline__ uint32_t encode_staged(const QArgs& a, int64_t c, int lane, float s, uint32_t t0b,
+                                                  const Staged& st, int64_t nfull) {
+  uint32_t todo = 0u;
+  if (t0b) {
+    const uint32_t mr[4] = {st.mr.x, st.mr.y, st.mr.z, st.mr.w};
+    uint32_t* wp = reinterpret_cast<uint32_t*>(a.slot) + (c * 128 + lane);  // row k's word: wp + 32 k
+    const bool full = c < nfull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool straddle;
+      const uint32_t w = staged_row_codes(t0b, mr[k], st.q[k], &straddle);
+      todo |= straddle ? 1u << k : 0u;
+      if (full) st_global_u32(wp + 32 * k, w);
+      else store_row_codes(a, c, k, lane, w, true);
+    }
+  } else if (!(s > 0.0f) || !(s <= FLT_MAX)) {  // zero or non-finite scale: every code 0
+#pragma unroll
+    for (int k = 0; k < 4; ++k) store_row_codes(a, c, k, lane, 0u, c >= nfull);
+  } else {
+    todo = 16u;
+  }
+  if (a.stg_hints & 2) {  // the chunk's 2 KB of summaries are dead: drop them from L2 without a write-back
+    __syncwarp();
+    if (lane < 16) asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.stg + c * 512 + 32 * lane) : "memory");
+  }
+  return todo;
+}
+
+// Exact codes of one row of 8 elements from theta and A (the fast-path
+// encode is exact given Delta), overwriting the word pass 2 stored.
+__device__ __forceinline__ void fix_row(const QArgs& a, int64_t r, uint32_t t0b) {
+  const int64_t e0 = 8 * r;
+  uint32_t w = 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t idx = e0 + i;
+    const uint32_t code = idx < a.n ? encode_fast(__fsub_rn(a.anchor[idx], a.theta[idx]), t0b + 0x7fffffu) : 0u;
+    w |= code << (4 * i);
+  }
+  if (4 * (size_t)r < a.scales_off) reinterpret_cast<uint32_t*>(a.slot)[r] = w;  // past n: padding words hold 0
+}
+
+// After the chunk loop (nothing else live): bit 4 (warp-uniform) re-reads
+// the whole chunk; the straddling rows (bits 0-3 of each lane) are
+// re-encoded in place.  (Deferring them to a fix-up kernel through a list
+// measured the same: the kernel's 6-8 us ate what pass 2 saved.)
+__device__ __forceinline__ void finish_staged(const QArgs& a, int64_t c, int lane, uint32_t t0b, uint32_t todo,
+                                              int64_t nfull) {
+  if (__any_sync(kFull, todo & 16u)) {
+    encode_chunk_call(a, c, lane, c < nfull);
+    return;
+  }
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k)
+    if ((todo >> k) & 1u) fix_row(a, (c * 1024 + 256 * k + 8 * lane) >> 3, t0b);
+}
+
+// The chunk's block scale s and bits(T_0(s)) for the fast path: normal
+// s >= 2^-100 (T_0 inline, e3m0_t0_normal; its T_6 is then normal); any other
+// s gets t0b = 0 and encode_staged's other branches.  Cached per block.
+__device__ __forceinline__ void staged_scale(const QArgs& a, int64_t c, int64_t& blk, float& s, uint32_t& t0b) {
+  const int64_t b = block_of_chunk(a, c);
+  if (b == blk) return;
+  blk = b;
+  s = reinterpret_cast<const float*>(a.slot + a.scales_off)[b];
+  uint32_t t = 0u;
+  if (s >= 0x1p-100f && s <= FLT_MAX) {
+    const float t0 = e3m0_t0_normal(s);
+    t = fast_ok(s, t0) ? __float_as_uint(t0) : 0u;
+  }
+  t0b = t;
+}
+
+// kStagedCpw chunks per warp, 4 resident CTAs per SM (<= 64 registers; measured against 1 chunk at 6
+// CTAs/SM, 4 at 2, a TMA-staged tile and a persistent grid: profiles/r2_b0_staged.txt)
+constexpr int kStagedCpw = 2;
+
+__global__ void __launch_bounds__(kThreads, 4) k_encode_staged(QArgs a) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kWpb = kThreads / 32;
+  const int64_t nfull = a.n >> 10;
+  const int64_t nchunks = nfull + ((nfull << 10) < a.n ? 1 : 0);
+  // tile b = chunks [top - 8 kStagedCpw, top), top = nchunks - b * 8 kStagedCpw; chunk j of warp w: top - 1 - w - 8 j
+  const int64_t top = nchunks - (int64_t)blockIdx.x * (kWpb * kStagedCpw) - 1 - (threadIdx.x >> 5);
+  // every load first, then per chunk its block's T_0 (inline, cached per block) and the codes,
+  // then the rare exact re-encodes (nothing else live)
+  Staged x[kStagedCpw];
+#pragma unroll
+  for (int j = 0; j < kStagedCpw; ++j)
+    if (top - kWpb * j >= 0) load_staged(a, top - kWpb * j, lane, x[j]);
+  int64_t blk = -1;
+  float s = 0.0f;
+  uint32_t t0b = 0u, t0s[kStagedCpw], todo[kStagedCpw];
+#pragma unroll
+  for (int j = 0; j < kStagedCpw; ++j) {
+    const int64_t c = top - kWpb * j;
+    todo[j] = 0u;
+    t0s[j] = 0u;
+    if (c < 0) continue;
+    staged_scale(a, c, blk, s, t0b);
+    t0s[j] = t0b;
+    todo[j] = encode_staged(a, c, lane, s, t0b, x[j], nfull);
+  }
+#pragma unroll
+  for (int j = 0; j < kStagedCpw; ++j)
+    if (__any_sync(kFull, todo[j] != 0u)) finish_staged(a, top - kWpb * j, lane, t0s[j], todo[j], nfull);
   if (blockIdx.x == 0) write_tail(a);
   if (a.sig) signal_round(a);
 }
@@ -713,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_adamw_quantize(QArgs a, AdamArg
 // block max accumulated in the same pass, so the inner step before a send
 // costs 32 + 8.5 B/param (k_encode re-reads theta and A) instead of
 // 28 + 16.5 with a separate absmax pass.
-template <bool kFullChunk>
+template <bool kFullChunk, bool kStage, bool kEF>
 __device__ __forceinline__ void adamw_absmax_chunk(const QArgs& a, const AdamArgs& h, int64_t c, int lane,
                                                    int64_t& cur, uint32_t& run) {
   // row by row (no Delta kept past its row): the block max and the first
@@ -725,8 +1022,9 @@ __device__ __forceinline__ void adamw_absmax_chunk(const QArgs& a, const AdamArg
     const int64_t e = e0 + 256 * k;
     float d[8];
     if (kFullChunk) {
-      f8 t = ld8(h.theta + e), g = ld8_stream(h.grad + e), m = ld8(h.m + e), v = ld8(h.v + e);
-      const f8 an = ld8_stream(a.anchor + e);
+      f8 t = ld8(h.theta + e), g = kEF ? ld8_stream_ef(h.grad + e) : ld8_stream(h.grad + e), m = ld8(h.m + e),
+         v = ld8(h.v + e);
+      const f8 an = kEF ? ld8_stream_ef(a.anchor + e) : ld8_stream(a.anchor + e);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         adamw_one(t.v[j], g.v[j], m.v[j], v.v[j], h);
@@ -749,14 +1047,21 @@ __device__ __forceinline__ void adamw_absmax_chunk(const QArgs& a, const AdamArg
         }
       }
     }
+    uint32_t rm = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {  // rows ascending, then j ascending: the lane's first bad index
       const uint32_t ab = abs_bits(d[j]);
-      mx = max(mx, ab);
+      rm = max(rm, ab);
       if (ab >= kInfBits && bad == 0xffffffffu) bad = (uint32_t)(256 * k + 8 * lane + j);
     }
+    if (kStage) {
+      rm = __reduce_max_sync(kFull, rm);
+      stage_row(a, c, k, lane, d, rm);
+      if (lane == k) a.stg_max[4 * c + k] = rm;
+    }
+    mx = max(mx, rm);
   }
-  const uint32_t m = __reduce_max_sync(kFull, mx);
+  const uint32_t m = kStage ? mx : __reduce_max_sync(kFull, mx);
   if (m >= kInfBits) {  // index of the first non-finite Delta of the chunk (as record_first_bad)
     const uint32_t b = __reduce_min_sync(kFull, bad);
     if (lane == 0 && b != 0xffffffffu)
@@ -771,6 +1076,7 @@ __device__ __forceinline__ void adamw_absmax_chunk(const QArgs& a, const AdamArg
   run = max(run, m);
 }
 
+template <bool kStage, bool kEF>
 __global__ void __launch_bounds__(kThreads, 3) k_adamw_absmax(QArgs a, AdamArgs h) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -778,8 +1084,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_adamw_absmax(QArgs a, AdamArgs 
   const int64_t nfull = a.n >> 10;
   int64_t cur = -1;
   uint32_t run = 0;
-  for (int64_t c = warp; c < nfull; c += nwarps) adamw_absmax_chunk<true>(a, h, c, lane, cur, run);
-  if ((nfull << 10) < a.n && warp == nfull % nwarps) adamw_absmax_chunk<false>(a, h, nfull, lane, cur, run);
+  for (int64_t c = warp; c < nfull; c += nwarps) adamw_absmax_chunk<true, kStage, kEF>(a, h, c, lane, cur, run);
+  if ((nfull << 10) < a.n && warp == nfull % nwarps)
+    adamw_absmax_chunk<false, kStage, kEF>(a, h, nfull, lane, cur, run);
   flush_block_max(a, lane, cur, run);
 }
 
@@ -1020,6 +1327,7 @@ int grid_for(K kernel, int num_sms, int64_t work_items, int items_per_block) {
   return g < 1 ? 1 : (int)g;
 }
 
+
 }  // namespace
 
 namespace {
@@ -1057,6 +1365,10 @@ QArgs make_qargs(const float* theta, const float* anchor, const Payload& pl, uin
   a.flags_off = rd.flags_off;
   a.seq = (unsigned long long)rd.seq;
   a.counter = rd.counter;
+  a.stg = nullptr;
+  a.stg_max = nullptr;
+  a.stg_hints = 0;
+  a.stg_keep_from = INT64_MAX;
   return a;
 }
 
@@ -1078,33 +1390,87 @@ namespace {
 // is built locally; in push mode the finished slot is then pushed (and the
 // round signalled) by k_push_copy.  Pass 1 is k_absmax, or k_adamw_absmax
 // when an AdamW step is fused in (h != nullptr).
+// Staging hints (SD_STAGE_HINTS, measurement switch; default both): bit 0
+// pass 1 reads theta, A (and g) evict-first in L2, so the summaries it
+// writes stay there for pass 2; bit 1 pass 2 discards the summaries it has
+// consumed (no write-back of dead lines).
+int stage_hints() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_STAGE_HINTS");
+    v = e ? (atoi(e) & 3) : 3;
+  }
+  return v;
+}
+
+// MB of summaries kept in L2 between the passes (SD_STAGE_L2_MB, measurement switch; default 40)
+int stage_keep_mb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_STAGE_L2_MB");
+    v = e ? atoi(e) : 40;
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
+template <bool kStage, bool kEF>
+void launch_pass1(const QArgs& a, const AdamArgs* h, int g, cudaStream_t st) {
+  if (h)
+    k_adamw_absmax<kStage, kEF><<<g, kThreads, 0, st>>>(a, *h);
+  else
+    k_absmax<kStage, kEF><<<g, kThreads, 0, st>>>(a);
+}
+
 int two_pass(const QArgs& a, const Round& rd, const Payload& pl, uint8_t* slot, int num_sms, cudaStream_t st,
-             const AdamArgs* h) {
+             const AdamArgs* h, const Workspace& ws) {
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int wpb = kThreads / 32;
   QArgs loc = a;
   loc.push = 0;
   loc.sig = a.sig && !a.push;
+  if (ws.ptr && ws.bytes >= stage_bytes(pl.n) && chunks > 0) {
+    loc.stg = reinterpret_cast<uint32_t*>(ws.ptr);
+    loc.stg_max = reinterpret_cast<uint32_t*>(ws.ptr + 2048 * (size_t)chunks);
+    loc.stg_hints = stage_hints();
+    // the last stage_keep_mb() MB of summaries pass 1 writes stay in L2 for pass 2 (which starts there and
+    // discards them: no write-back) -- only with the discard hint, or they would linger as evict-last lines
+    if (loc.stg_hints & 2) loc.stg_keep_from = chunks - (int64_t)stage_keep_mb() * (1 << 20) / 2048;
+  }
   if (pl.nb > 0 && cudaMemsetAsync(slot + pl.scales_off, 0, 4 * (size_t)pl.nb, st) != cudaSuccess) return -1;
   QArgs pass1 = loc;
   pass1.sig = 0;
-  if (h)
-    k_adamw_absmax<<<grid_for(k_adamw_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1, *h);
+  const int g1 = grid_for(k_absmax<false, false>, num_sms, chunks, wpb);
+  if (!loc.stg)
+    launch_pass1<false, false>(pass1, h, g1, st);
+  else if (loc.stg_hints & 1)
+    launch_pass1<true, true>(pass1, h, g1, st);
   else
-    k_absmax<<<grid_for(k_absmax, num_sms, chunks, wpb), kThreads, 0, st>>>(pass1);
-  k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
+    launch_pass1<true, false>(pass1, h, g1, st);
+  if (loc.stg) {
+    const int64_t g = (chunks + wpb * kStagedCpw - 1) / (wpb * kStagedCpw);  // one CTA per tile (>= 1: write_tail)
+    k_encode_staged<<<g < 1 ? 1 : (int)g, kThreads, 0, st>>>(loc);
+  } else {
+    k_encode<<<grid_for(k_encode, num_sms, chunks, wpb), kThreads, 0, st>>>(loc);
+  }
   int launched = 2;
   if (a.push) {
     k_push_copy<<<grid_for(k_push_copy, num_sms, (int64_t)(pl.bytes / 16), kThreads), kThreads, 0, st>>>(a);
-    launched = 3;
+    ++launched;
   }
   launched += maybe_signal(rd, a, st);
   return cudaGetLastError() == cudaSuccess ? launched : -1;
 }
 }  // namespace
 
+// [chunks x 2 KB summaries][chunks x 16 B row maxima]
+size_t stage_bytes(int64_t n) {
+  const int64_t chunks = n > 0 ? (n + 1023) >> 10 : 0;
+  return (size_t)chunks * (2048 + 16);
+}
+
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Round& rd,
-                    int num_sms, cudaStream_t st) {
+                    int num_sms, cudaStream_t st, const Workspace& ws) {
   const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int wpb = kThreads / 32;
@@ -1116,7 +1482,7 @@ int launch_quantize(const float* theta, const float* anchor, const Payload& pl, 
     const int ks = maybe_signal(rd, a, st);
     return cudaGetLastError() == cudaSuccess ? 1 + ks : -1;
   }
-  return two_pass(a, rd, pl, slot, num_sms, st, nullptr);
+  return two_pass(a, rd, pl, slot, num_sms, st, nullptr, ws);
 }
 
 int launch_round_wait(const RoundRecv& rr, const Payload& pl, int M, uint64_t timeout_ns, unsigned long long* status,
@@ -1170,10 +1536,11 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 }
 
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
-                          uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st) {
+                          uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st,
+                          const Workspace& ws) {
   const QArgs a = make_qargs(theta, anchor, pl, slot, rd);
   const AdamArgs h = make_adam(theta, grad, m, v, pl.n, hp);
-  if (!single_pass(pl.B)) return two_pass(a, rd, pl, slot, num_sms, st, &h);  // AdamW + block max, then encode
+  if (!single_pass(pl.B)) return two_pass(a, rd, pl, slot, num_sms, st, &h, ws);  // AdamW + block max, then encode
   const int64_t chunks = (pl.n + 1023) >> 10;
   const int g = grid_for(k_adamw_quantize<1>, num_sms, chunks > 0 ? chunks : 1, kThreads / 32);
   if (pl.B == 1024)

@@ -32,12 +32,22 @@ struct Round {
   bool push = false;
 };
 
+// Caller workspace of the two-pass quantize (B = 0 or B > 1024): with at
+// least stage_bytes(n) bytes (256-aligned) pass 1 leaves 16-bit summaries of
+// the Deltas there and pass 2 encodes from them instead of re-reading theta
+// and A.  Empty: pass 2 re-reads.
+struct Workspace {
+  uint8_t* ptr = nullptr;
+  size_t bytes = 0;
+};
+size_t stage_bytes(int64_t n);
+
 // Delta = anchor - theta, per-block absmax, exact E3M0, nibble pack, trailer
 // (+ the round signal).  slot: one payload (256-aligned).  The trailer's
 // first_bad word must hold 2^64-1 before the launch (sd_outer_grad_quantize
 // memsets it).  Returns the number of kernels launched, or -1.
 int launch_quantize(const float* theta, const float* anchor, const Payload& pl, uint8_t* slot, const Round& rd,
-                    int num_sms, cudaStream_t st);
+                    int num_sms, cudaStream_t st, const Workspace& ws = Workspace());
 
 // Receive side of the fused all-gather: this half's flag entries (local),
 // this rank's own slot, and in pull mode the window to reach the peers'
@@ -79,7 +89,8 @@ int launch_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
 // (single pass for B in {256, 512, 1024}; otherwise AdamW fused with the first
 // pass -- the block max -- then k_encode).
 int launch_adamw_quantize(float* theta, const float* grad, float* m, float* v, const float* anchor, const Payload& pl,
-                          uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st);
+                          uint8_t* slot, const AdamHyper& hp, const Round& rd, int num_sms, cudaStream_t st,
+                          const Workspace& ws = Workspace());
 
 // Fused decode + M-way fp32 mean + Nesterov + anchor update + alpha-merge.
 // status: host-mapped pinned words {first_bad, code, dead} (code written

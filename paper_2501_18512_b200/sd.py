@@ -29,7 +29,7 @@ EXPORTS = (
     "sd_fragment_schedule", "sd_num_scale_blocks", "sd_payload_bytes", "sd_payload_scales_offset",
     "sd_payload_trailer_offset", "sd_get_unique_id", "sd_init", "sd_gather_alloc", "sd_gather_free", "sd_set_gather_mode",
     "sd_gather_payloads",
-    "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync", "sd_comm_stream",
+    "sd_quantize_workspace_bytes", "sd_set_workspace", "sd_outer_state_init", "sd_state_prefetch", "sd_state_writeback", "sd_state_sync", "sd_comm_stream",
     "sd_inner_adamw", "sd_inner_adamw_quantize", "sd_inner_adamw_merge", "sd_outer_grad_quantize", "sd_fragment_sync", "sd_fragment_wait", "sd_merge", "sd_check", "sd_last_error",
     "sd_finalize", "sd_kernel_launch_count",
 )
@@ -85,6 +85,8 @@ def lib():
             "sd_gather_free": ([P, P], I32),
             "sd_set_gather_mode": ([P, I32], I32),
             "sd_gather_payloads": ([P, I32, P, ctypes.POINTER(P)], I32),
+            "sd_quantize_workspace_bytes": ([C, I64], SZ),
+            "sd_set_workspace": ([P, P, SZ], I32),
             "sd_outer_state_init": ([P, P, P, P, I64, P], I32),
             "sd_state_prefetch": ([P, I32, P, P, P, P, I64, P], I32),
             "sd_state_writeback": ([P, I32, P, P, P, P, I64, P], I32),
@@ -181,6 +183,10 @@ def sd_payload_trailer_offset(cfg: SdConfig, n: int) -> int:
     return lib().sd_payload_trailer_offset(ctypes.byref(cfg), n)
 
 
+def sd_quantize_workspace_bytes(cfg: SdConfig, n: int) -> int:
+    return lib().sd_quantize_workspace_bytes(ctypes.byref(cfg), n)
+
+
 def sd_kernel_launch_count() -> int:
     return lib().sd_kernel_launch_count()
 
@@ -273,6 +279,16 @@ class SdContext:
         out = ctypes.c_void_p(0)
         self._c(lib().sd_comm_stream(self.h, ctypes.byref(out)))
         return out.value or 0
+
+    def sd_set_workspace(self, ws, nbytes=None):
+        """ws: a device tensor (or None to detach); the ctx keeps a reference while attached"""
+        if ws is None:
+            self._ws = None
+            self._c(lib().sd_set_workspace(self.h, None, 0))
+            return
+        nbytes = ws.numel() * ws.element_size() if nbytes is None else nbytes
+        self._c(lib().sd_set_workspace(self.h, _ptr(ws), nbytes))
+        self._ws = ws
 
     def sd_outer_state_init(self, theta, anchor, momentum, n=None, stream=None):
         n = theta.numel() if n is None else n

@@ -30,6 +30,14 @@ class FragmentSync:
         self.ctx = sd.SdContext(cfg, rank, world, unique_id if world > 1 else None, device)
         self.payload = [sd.sd_payload_bytes(cfg, n) for n in self.n]
         self.ctx.sd_set_gather_mode(gather_mode)
+        # scratch of the two-pass quantize (B = 0 or B > 1024): one for all fragments (sends are stream-ordered)
+        ws = max([sd.sd_quantize_workspace_bytes(cfg, n) for n in self.n] + [0])
+        self.workspace = None
+        if ws > 0:
+            import torch
+
+            self.workspace = torch.empty(ws, dtype=torch.uint8, device=torch.device("cuda", device))
+            self.ctx.sd_set_workspace(self.workspace)
         # libsd-owned gather buffers: NCCL symmetric memory (copy-engine all-gather, zero SMs)
         # with a communicator; plain device memory otherwise
         self.gather = []

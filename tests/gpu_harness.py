@@ -27,11 +27,19 @@ class EmulatedReplicas:
     """M replicas of one fragment on cuda:0, each with its own copy of the
     (replicated) anchor and momentum, as on M separate GPUs."""
 
-    def __init__(self, cfg, M: int, n: int):
+    def __init__(self, cfg, M: int, n: int, staged: bool = True):
+        """staged: give every replica's ctx its own quantize workspace (the
+        two-pass quantize then encodes from 16-bit summaries; as FragmentSync
+        does); False: no workspace (the second pass re-reads theta and A)."""
         self.cfg, self.M, self.n = cfg, M, n
         self.pb = sd.sd_payload_bytes(cfg, n)
         self.ctx = [sd.SdContext(cfg, m, M, None, 0) for m in range(M)]
         self.gather = torch.empty(M * self.pb, dtype=torch.uint8, device=DEV)
+        ws = sd.sd_quantize_workspace_bytes(cfg, n)
+        if staged and ws > 0:
+            for c in self.ctx:
+                # garbage: nothing may depend on the workspace's previous contents
+                c.sd_set_workspace(torch.full((ws,), 0xC5, dtype=torch.uint8, device=DEV))
 
     def slot(self, m):
         return self.gather[m * self.pb:(m + 1) * self.pb]

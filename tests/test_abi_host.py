@@ -112,3 +112,18 @@ def test_schedule_rejects_step_zero():
     c = sd.sd_config_default(24, 3, 100)
     with pytest.raises(sd.SdError, match="must be >= 1"):
         sd.sd_fragment_schedule(c, 0)
+
+
+def test_quantize_workspace_bytes():
+    """Scratch only for the two-pass quantize (B = 0 or B > 1024): 2 bytes of
+    summary per element plus one 16-byte row-max record per 1024-element chunk."""
+    for B in (256, 512, 1024):
+        assert sd.sd_quantize_workspace_bytes(sd.sd_config_default(2, 1, 10, scale_block=B), 10 ** 6) == 0
+    for B in (0, 2048, 1 << 20):
+        c = sd.sd_config_default(2, 1, 10, scale_block=B)
+        assert sd.sd_quantize_workspace_bytes(c, 0) == 0
+        assert sd.sd_quantize_workspace_bytes(c, 1) == 2064
+        assert sd.sd_quantize_workspace_bytes(c, 1024) == 2064
+        assert sd.sd_quantize_workspace_bytes(c, 1025) == 2 * 2064
+        assert sd.sd_quantize_workspace_bytes(c, 151007616) == 147469 * 2064
+    assert sd.sd_quantize_workspace_bytes(sd.sd_config_default(2, 1, 10, scale_block=3000), 4096) == 0  # invalid B

@@ -43,15 +43,19 @@ def cfg_for(B, alpha=0.5, lr=0.4, mu=0.9, tau=1):
 
 
 # ------------------------------------------------------------------ quantize
-@pytest.mark.parametrize("B", [0, 256, 512, 1024, 2048, 65536])
+@pytest.mark.parametrize("B,staged", [(0, True), (0, False), (256, True), (512, True), (1024, True), (2048, True),
+                                      (2048, False), (65536, True), (65536, False)])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 1023, 1024, 1025, 4097, 33 * 1024 + 511, 262144 + 3])
-def test_quantize_payload_bytes_match(n, B):
+def test_quantize_payload_bytes_match(n, B, staged):
+    """staged: the two-pass quantize (B = 0, 2048, 65536) with a workspace
+    (encode from 16-bit summaries, exact re-read at straddled thresholds) and
+    without one (re-read); the single-pass B's ignore it."""
     rng = np.random.default_rng(n * 7 + B)
     cfg = cfg_for(B)
     for exact in (True, False):
         delta = edge_deltas(n, B, rng)
         A, th = theta_anchor_for(delta, rng, exact)
-        rep = EmulatedReplicas(cfg, 1, n)
+        rep = EmulatedReplicas(cfg, 1, n, staged=staged)
         rep.slot(0).fill_(0xAB)  # garbage: every byte must be written
         rep.quantize_all(0, 10, [to_dev(th)], [to_dev(A)])
         torch.cuda.synchronize()
@@ -60,6 +64,74 @@ def test_quantize_payload_bytes_match(n, B):
         assert not poisoned
         diff = np.nonzero(got != want)[0]
         assert diff.size == 0, f"n={n} B={B} exact={exact}: {diff.size} bytes differ, first at {diff[:8]}"
+        rep.close()
+
+
+@pytest.mark.parametrize("B", [0, 4096])
+@pytest.mark.parametrize("n", [256 * 1024 + 77, 3 * 1024 * 1024 + 5])
+def test_quantize_staged_buckets(n, B):
+    """The staged two-pass quantize against the oracle where its 16-bit
+    summaries are tested hardest: rows (256 elements) whose maxima sit 0..8
+    octaves below the block scale s (so the summary's base moves), every
+    value within +-6 ulps of a threshold T_j(s) = s 2^(-j-1/2) that lies
+    below its row's max (so most buckets straddle or touch a threshold and
+    take the exact re-read), values below 2^-7 of the row max, and -0 / +0."""
+    from decimal import Decimal
+
+    rng = np.random.default_rng(n + B)
+    blen = B if B else n
+    d = np.zeros(n, np.float32)
+    for b0 in range(0, n, blen):
+        s = np.float32(rng.uniform(0.5, 2.0) * 2.0 ** int(rng.integers(-20, 20)))
+        T = [np.float32(float(Decimal(float(s)) * (Decimal(2) ** Decimal(-j - 0.5)))) for j in range(7)]
+        for r0 in range(b0, min(n, b0 + blen), 256):
+            r1 = min(n, r0 + 256, b0 + blen)
+            oct_ = int(rng.integers(0, 9))
+            j = rng.integers(min(oct_, 6), 7, r1 - r0)
+            tb = np.array([int(T[k].view(np.uint32)) for k in j], np.int64) + rng.integers(-6, 7, r1 - r0)
+            vals = tb.astype(np.uint32).view(np.float32) * np.where(rng.random(r1 - r0) < 0.5, 1, -1).astype(np.float32)
+            low = rng.random(r1 - r0) < 0.2  # far below the row max
+            vals[low] = (s * np.float32(2.0 ** -(oct_ + 8)) * rng.random(int(low.sum()))).astype(np.float32)
+            vals[rng.random(r1 - r0) < 0.05] = -0.0
+            vals[0] = np.float32(s * np.float32(2.0 ** -oct_))  # the row max
+            d[r0:r1] = vals
+        d[b0 + int(rng.integers(0, min(blen, n - b0)))] = s  # the block max
+    A, th = theta_anchor_for(d, rng, True)
+    rep = EmulatedReplicas(cfg_for(B), 1, n, staged=True)
+    rep.quantize_all(0, 10, [to_dev(th)], [to_dev(A)])
+    torch.cuda.synchronize()
+    want, poisoned = oracle.quantize(th, A, B)
+    got = rep.gather.cpu().numpy()
+    assert not poisoned
+    diff = np.nonzero(got != want)[0]
+    assert diff.size == 0, f"{diff.size} bytes differ, first at {diff[:8]}"
+    rep.close()
+
+
+def test_quantize_workspace_rules():
+    """sd_set_workspace: a 256-byte-misaligned workspace is refused; one
+    smaller than sd_quantize_workspace_bytes(n) is not used (the re-reading
+    pass runs); detaching works; all give the oracle's payload."""
+    n, B = 5 * 1024 + 3, 0
+    cfg = cfg_for(B)
+    need = sd.sd_quantize_workspace_bytes(cfg, n)
+    assert need == 6 * (2048 + 16)
+    rng = np.random.default_rng(3)
+    delta = edge_deltas(n, B, rng)
+    A, th = theta_anchor_for(delta, rng, False)
+    want, _ = oracle.quantize(th, A, B)
+    big = torch.zeros(need + 512, dtype=torch.uint8, device=DEV)
+    for ws, nbytes in ((big[1:], need), (big, need - 1), (big, need), (None, 0)):
+        rep = EmulatedReplicas(cfg, 1, n, staged=False)
+        if ws is not None and ws.data_ptr() % 256:
+            with pytest.raises(sd.SdError) as e:
+                rep.ctx[0].sd_set_workspace(ws, nbytes)
+            assert e.value.status == sd.SD_ERR_ARG and "aligned" in e.value.msg
+        else:
+            rep.ctx[0].sd_set_workspace(ws, nbytes)
+        rep.quantize_all(0, 10, [to_dev(th)], [to_dev(A)])
+        torch.cuda.synchronize()
+        assert np.array_equal(rep.gather.cpu().numpy(), want)
         rep.close()
 
 
@@ -517,10 +589,12 @@ def test_inner_adamw_bit_exact(n):
     ctx.sd_finalize()
 
 
-@pytest.mark.parametrize("B", [1024, 512, 256, 0, 4096])
+@pytest.mark.parametrize("B,staged", [(1024, True), (512, True), (256, True), (0, True), (0, False), (4096, True),
+                                      (4096, False)])
 @pytest.mark.parametrize("n", [1025, 64 * 1024 + 77])
-def test_inner_adamw_quantize_fused_bit_exact(n, B):
-    """The fused last-inner-step + quantize equals AdamW then or_quantize."""
+def test_inner_adamw_quantize_fused_bit_exact(n, B, staged):
+    """The fused last-inner-step + quantize equals AdamW then or_quantize
+    (B = 0 / 4096: AdamW + block max + staged summaries, or no workspace)."""
     rng = np.random.default_rng(n + B)
     A = (rng.standard_normal(n) * 0.02).astype(np.float32)
     th = (A - rng.standard_normal(n).astype(np.float32) * 1e-3).astype(np.float32)
@@ -528,7 +602,7 @@ def test_inner_adamw_quantize_fused_bit_exact(n, B):
     v = (rng.random(n) * 1e-7).astype(np.float32)
     g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
     cfg = cfg_for(B)
-    rep = EmulatedReplicas(cfg, 1, n)
+    rep = EmulatedReplicas(cfg, 1, n, staged=staged)
     hp = sd.SdAdamW(**HP)
     th_d, m_d, v_d = to_dev(th), to_dev(m), to_dev(v)
     rep.ctx[0].sd_inner_adamw_quantize(0, 10, 7, th_d, to_dev(g), m_d, v_d, to_dev(A), rep.slot(0), hp, n)
