@@ -548,12 +548,16 @@ __device__ __forceinline__ uint32_t gather_hi_nibbles(const uint32_t (&v)[4]) {
 }
 
 // The code word of one row of one lane; *straddle = some element needs the exact re-read.
-__device__ __forceinline__ uint32_t staged_row_codes(uint32_t t0bits, uint32_t row_max, const uint4& qv,
-                                                     bool* straddle) {
+// Row parameters (depend on the row max and T_0 only): Kpair = (K + 2^15)
+// in both halves, rho = (r_0 != 0).
+__device__ __forceinline__ uint32_t staged_row_kpair(uint32_t t0bits, uint32_t row_max, uint32_t* rho) {
   const uint32_t a0 = t0bits - stage_base(row_max);
-  const uint32_t rho = (a0 & 2047u) != 0u ? 1u : 0u;
-  const int K = max(32767 - (int)((a0 >> 11) + rho + 4095u), -32768);
-  const uint32_t Kpair = (uint32_t)(K + 32768) * 0x10001u;
+  *rho = (a0 & 2047u) != 0u ? 1u : 0u;
+  const int K = max(32767 - (int)((a0 >> 11) + *rho + 4095u), -32768);
+  return (uint32_t)(K + 32768) * 0x10001u;
+}
+
+__device__ __forceinline__ uint32_t staged_row_codes(uint32_t Kpair, bool rho, const uint4& qv, bool* straddle) {
   const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
   uint32_t v[4], acc = 0;
 #pragma unroll
@@ -657,13 +661,18 @@ __device__ __forceinline__ uint32_t encode_staged(const QArgs& a, int64_t c, int
                                                   const Staged& st, int64_t nfull) {
   uint32_t todo = 0u;
   if (t0b) {
-    const uint32_t mr[4] = {st.mr.x, st.mr.y, st.mr.z, st.mr.w};
+    // the 4 rows' parameters: lane k (mod 4) computes row k's, then broadcast
+    const int r = lane & 3;
+    const uint32_t mrl = r == 0 ? st.mr.x : r == 1 ? st.mr.y : r == 2 ? st.mr.z : st.mr.w;
+    uint32_t rho;
+    const uint32_t kp = staged_row_kpair(t0b, mrl, &rho);
+    const uint32_t rhos = __ballot_sync(kFull, rho != 0u);  // bit k: row k
     uint32_t* wp = reinterpret_cast<uint32_t*>(a.slot) + (c * 128 + lane);  // row k's word: wp + 32 k
     const bool full = c < nfull;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       bool straddle;
-      const uint32_t w = staged_row_codes(t0b, mr[k], st.q[k], &straddle);
+      const uint32_t w = staged_row_codes(__shfl_sync(kFull, kp, k), (rhos >> k) & 1u, st.q[k], &straddle);
       todo |= straddle ? 1u << k : 0u;
       if (full) st_global_u32(wp + 32 * k, w);
       else store_row_codes(a, c, k, lane, w, true);
