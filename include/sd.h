@@ -147,7 +147,9 @@ sd_status sd_get_unique_id(uint8_t id[SD_UNIQUE_ID_BYTES]);
  * emulation seam for M > 1: the caller then fills every slot of the gather
  * buffer itself (one ctx per emulated replica) and sd_fragment_sync only
  * orders streams.  id != NULL: collective over the M processes (blocking
- * NCCL communicator init).  Creates a highest-priority comm stream.  */
+ * NCCL communicator init; M == 1 included: a one-rank communicator runs the
+ * same gather paths, every one trivially).  Creates a highest-priority comm
+ * stream.  */
 sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, const uint8_t* id,
                   int32_t device);
 

@@ -381,7 +381,7 @@ sd_status sd_init(sd_ctx** out, const sd_config* cfg, int32_t rank, int32_t M, c
   c->status_host[2] = 0;
   e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->status_dev), c->status_host, 0);
   if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "cudaHostGetDevicePointer"));
-  if (id && M > 1) {
+  if (id) {  // M = 1 too: a one-rank communicator runs the same paths (tests)
     ncclUniqueId u;
     memcpy(u.internal, id, SD_UNIQUE_ID_BYTES);
     // copy-engine collectives on symmetric windows: the gather takes no SMs

@@ -858,7 +858,7 @@ __global__ void k_round_wait(WArgs w) {
   if (q < w.M && s_code != 3) {
     unsigned long long fb;
     int code = 0;
-    if (w.pull) {  // the apply addresses slot m as LSA(half, 0) + m (LSA stride + pb): check it
+    if (w.pull && w.M > 1) {  // the apply addresses slot m as LSA(half, 0) + m (LSA stride + pb): check it
       const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off, 0));
       const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off, 1));
       const uint8_t* bq = static_cast<const uint8_t*>(ncclGetLsaPointer(w.win, w.half_off + (size_t)q * w.pb, q));
@@ -1214,9 +1214,8 @@ __global__ void __launch_bounds__(kThreads, (kAdam && kM == 8) ? SD_APPLY_MINB_A
   size_t gs = p.pb;
   if (p.pull) {
     const uint8_t* b0 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 0));
-    const uint8_t* b1 = static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 1));
     gb = b0;
-    gs = (size_t)(b1 - b0) + p.pb;
+    if (M > 1) gs = (size_t)(static_cast<const uint8_t*>(ncclGetLsaPointer(p.win, p.half_off, 1)) - b0) + p.pb;
   }
   auto slot_of = [&](int m) -> const uint8_t* { return gb + (size_t)m * gs; };
 

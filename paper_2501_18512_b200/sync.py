@@ -14,20 +14,27 @@ from . import sd
 
 class FragmentSync:
     def __init__(self, cfg: sd.SdConfig, frag_numel, rank: int = 0, world: int = 1, device: int = 0,
-                 unique_id: bytes | None = None, gather_mode: int = sd.SD_GATHER_AUTO):
+                 unique_id: bytes | None = None, gather_mode: int = sd.SD_GATHER_AUTO,
+                 communicator: bool | None = None):
+        """communicator: give the context an NCCL communicator (default: world > 1).
+        True at world = 1 runs the communicator paths with one rank (tests)."""
         self.cfg = cfg
+        comm = world > 1 if communicator is None else bool(communicator)
         self.rank, self.world, self.device = rank, world, device
         self.P = sd.sd_fragment_count(cfg)
         if len(frag_numel) != self.P:
             raise ValueError(f"{len(frag_numel)} fragment sizes given, the config has P = {self.P}")
         self.n = [int(x) for x in frag_numel]
-        if world > 1 and unique_id is None:
-            import torch.distributed as dist
+        if comm and unique_id is None:
+            if world > 1:
+                import torch.distributed as dist
 
-            obj = [sd.sd_get_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            unique_id = obj[0]
-        self.ctx = sd.SdContext(cfg, rank, world, unique_id if world > 1 else None, device)
+                obj = [sd.sd_get_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                unique_id = obj[0]
+            else:
+                unique_id = sd.sd_get_unique_id()
+        self.ctx = sd.SdContext(cfg, rank, world, unique_id if comm else None, device)
         self.payload = [sd.sd_payload_bytes(cfg, n) for n in self.n]
         self.ctx.sd_set_gather_mode(gather_mode)
         # scratch of the two-pass quantize (B = 0 or B > 1024): one for all fragments (sends are stream-ordered)

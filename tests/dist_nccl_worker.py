@@ -39,7 +39,9 @@ def main():
     _, t_p, _ = sd.sd_fragment_layout(cfg, p)
     mode = {"push": sd.SD_GATHER_PUSH, "pull": sd.SD_GATHER_PULL}.get(
         os.environ.get("SD_TEST_GATHER"), sd.SD_GATHER_COPY_ENGINE)
-    fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode)
+    # SD_TEST_COMM=1: a communicator even at world = 1 (the one-rank gather paths, runnable on one GPU)
+    fsync = FragmentSync(cfg, [n] * P, rank, world, local, gather_mode=mode,
+                         communicator=True if os.environ.get("SD_TEST_COMM") == "1" else None)
     if os.environ.get("SD_TEST_TORCH_BUF") == "1":  # caller-owned (non-symmetric) gather buffers
         fsync.gather = [torch.empty(world * pb, dtype=torch.uint8, device=dev) for pb in fsync.payload]
     A = synth.dev_init(torch.empty(n, device=dev), segs, p)

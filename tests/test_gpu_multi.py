@@ -23,16 +23,31 @@ def _free_port():
     return port
 
 
-def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False, offload=False, tiny=None):
+def _run(nproc, B, torch_buf=False, gather="ce", tau_per_rank=False, poison=False, offload=False, tiny=None,
+         comm=False):
     env = dict(os.environ, SD_TEST_B=str(B), SD_TEST_TORCH_BUF="1" if torch_buf else "0", SD_TEST_GATHER=gather,
                SD_TEST_TAU_PER_RANK="1" if tau_per_rank else "0", SD_TEST_POISON="1" if poison else "0",
-               SD_TEST_OFFLOAD="1" if offload else "0")
+               SD_TEST_OFFLOAD="1" if offload else "0", SD_TEST_COMM="1" if comm else "0", SD_LOG_INIT="1")
     if tiny is not None:
         env["SD_TEST_TINY"] = str(tiny)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "dist_nccl_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     return r.returncode, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("gather", ["ce", "push", "pull"])
+@pytest.mark.parametrize("B,poison", [(1024, False), (0, False), (1024, True)])
+def test_one_rank_communicator_bit_exact(gather, B, poison):
+    """The communicator paths with one rank (runs on a single GPU): NCCL
+    communicator, symmetric-window gather buffer, the copy-engine all-gather
+    on the comm stream ordered by events, or the fused push / pull protocol
+    (round signal by the payload kernel's last CTA, k_round_wait's verdict,
+    the pull apply's LSA addressing) -- each trivially, with no peer; 5 rounds
+    against the oracle, the last one poisoned in the poison case."""
+    rc, out = _run(1, B, gather=gather, poison=poison, comm=True)
+    assert rc == 0 and "OK" in out, out[-3000:]
+    assert "[libsd] rank 0/1: NCCL communicator up" in out and "fused gathers available" in out, out[-3000:]
 
 
 @pytest.mark.parametrize("B,torch_buf", [(1024, False), (0, False), (1024, True)])
