@@ -12,4 +12,4 @@ for G in ce push pull; do
 done
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --timeline gpurun_out/timeline_${TAG}_n4.json > gpurun_out/bench4_${TAG}.json 2> gpurun_out/bench4_${TAG}.err; echo "bench rc=$?"
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --workload 4B --steps 128 --no-e2e > gpurun_out/bench4_${TAG}_4B.json 2> gpurun_out/bench4_${TAG}_4B.err; echo "bench 4B rc=$?"
-[ "${SWEEP:-0}" = 1 ] && timeout 1500 bash scripts/gpu_sweep_multi.sh 4
+if [ "${SWEEP:-0}" = 1 ]; then timeout 1500 bash scripts/gpu_sweep_multi.sh 4; fi

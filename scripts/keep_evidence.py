@@ -26,9 +26,11 @@ if os.path.exists(j):
 names = {1: [(f"bench1_{tag}.json", "bench_n1.json"), (f"bench1s_{tag}.json", "bench_n1_driver_form.json"),
              (f"bench1ref_{tag}.json", "bench_n1_reference.json"), (f"bench1_{tag}_toy.json", "bench_toy_n1.json"),
              (f"bench1_{tag}_35M.json", "bench_35M_n1.json"), (f"smoke_{tag}.log", "smoke_final.log")],
-         2: [(f"bench2_{tag}.json", "bench_n2.json"), (f"timeline_{tag}_n2.json", "timeline_n2_tau5.json")],
+         2: [(f"bench2_{tag}.json", "bench_n2.json")],
          4: [(f"bench4_{tag}.json", "bench_n4.json"), (f"bench4_{tag}_4B.json", "bench_n4_4B.json"),
-             (f"timeline_{tag}_n4.json", "timeline_n4_tau5.json"), (f"soak_{tag}_n4.txt", "soak_final_n4.txt")]}
+             (f"soak_{tag}_n4.txt", "soak_final_n4.txt")]}
+for kind in ("adamw", "gemm", "pull_adamw", "pull_gemm"):  # bench.py --timeline: one Chrome trace per inner kind
+    names[n].append((f"timeline_{tag}_n{n}_{kind}.json", f"timeline_n{n}_tau5_{kind}.json"))
 for a, b in names[n]:
     p = os.path.join(src, a)
     if not os.path.exists(p):
