@@ -8,7 +8,7 @@ timeout 2700 python -m pytest tests -m gpu -q -rs --junitxml=gpurun_out/junit_${
 : > gpurun_out/soak_${TAG}_n4.txt
 for G in ce push pull; do
   SD_TEST_GATHER=$G SD_TEST_ROUNDS=2000 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29541 tests/dist_soak_worker.py > gpurun_out/soak_${TAG}_$G.log 2>&1
-  echo "$G 2000 rounds: rc=$? $(grep -c '^OK' gpurun_out/soak_${TAG}_$G.log) OK line(s)" | tee -a gpurun_out/soak_${TAG}_n4.txt
+  echo "$G 2000 rounds: rc=$? $(grep -c "rounds: OK" gpurun_out/soak_${TAG}_$G.log) OK line(s)" | tee -a gpurun_out/soak_${TAG}_n4.txt
 done
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --timeline gpurun_out/timeline_${TAG}_n4.json > gpurun_out/bench4_${TAG}.json 2> gpurun_out/bench4_${TAG}.err; echo "bench rc=$?"
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --workload 4B --steps 128 --no-e2e > gpurun_out/bench4_${TAG}_4B.json 2> gpurun_out/bench4_${TAG}_4B.err; echo "bench 4B rc=$?"
