@@ -8,8 +8,10 @@
 //   k_apply     Alg. 2 L8 receive side + L12 + L13
 //               decode, M-way fp32 sum in ascending replica order, /M,
 //               Nesterov, anchor update, alpha-merge.
-//   k_absmax + k_encode: the two-pass variant for B = 0 (one scale per
-//               fragment) and B > 1024.
+//   k_absmax + k_encode_staged (k_encode without a workspace): the two-pass
+//               variant for B = 0 (one scale per fragment) and
+//               B > 1024 -- pass 1 keeps 16-bit summaries of the Deltas in
+//               the caller's workspace, pass 2 encodes from them.
 // Around them: the fused all-gather protocol (push: NVLink stores from the
 // quantize; pull: NVLink loads in the apply; round flags signalled by the
 // payload kernel's last CTA or a one-thread kernel, k_round_wait for the
@@ -573,22 +575,6 @@ __device__ __forceinline__ uint32_t staged_row_codes(uint32_t Kpair, bool rho, c
   return (n ^ sg ^ 0x88888888u) & M;                                            // (n & 7) | sign << 3
 }
 
-// Exact codes for the straddling elements of a row (rare).
-__device__ __forceinline__ uint32_t staged_row_fixup(const float* __restrict__ theta, const float* __restrict__ anchor,
-                                                  int64_t n, int64_t e0, uint32_t t0bits, uint32_t row_max, uint4 qv,
-                                                  uint32_t w) {
-  const uint32_t a0 = t0bits - stage_base(row_max);
-  const uint32_t q0 = a0 >> 11;
-  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t u = (qw[i >> 1] >> (16 * (i & 1))) & 0x7fffu;
-    if (((u ^ q0) & 0xfffu) != 0u) continue;
-    const int64_t idx = e0 + i;
-    const uint32_t code = idx < n ? encode_fast(__fsub_rn(anchor[idx], theta[idx]), t0bits + 0x7fffffu) : 0u;
-    w = (w & ~(0xfu << (4 * i))) | (code << (4 * i));
-  }
-  return w;
-}
 
 // Pass 2 without a workspace: re-reads theta and A (k_encode), last chunk
 // first (pass 1 streamed the fragment forward, so its tail is what the L2
