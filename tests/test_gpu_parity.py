@@ -6,6 +6,8 @@ byte-identical; anchor, momentum and live parameters are bit-identical
 sequence), with the floored 1e-6 relative check of BASELINE.json's
 north_star as the stated tolerance.  Inputs: seeded synthetic data shaped
 like the paper's Chinchilla fragments (synth/) plus codec edge cases."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -385,6 +387,73 @@ def test_full_size_sampled_blocks(shape):
             assert_same(Acopies[m][lo:hi], Ao, f"block {b} anchor")
             assert_same(v_d[m][lo:hi], vo, f"block {b} momentum")
             assert_same(th_d[m][lo:hi], merges[m], f"block {b} theta")
+    rep.close()
+
+
+@pytest.mark.parametrize("adamw", [False, True])
+def test_full_size_b0_staged_whole_fragment(adamw):
+    """SPEC's B = 0 (one scale per fragment) at the full 1B fragment
+    size (n = 151,007,616) in the bench's launch configuration: the staged
+    two-pass quantize with its workspace (FragmentSync's), M = 2 emulated.
+    One scale depends on the whole fragment, so nothing short of the whole
+    round is checked: both payloads byte for byte (76 MB each) and A, v,
+    theta element for element against the oracle's full round (OpenMP
+    build, bit-identical to the single-thread one).  adamw: the send goes
+    through sd_inner_adamw_quantize (AdamW + block max + summaries, then the
+    encode pass), against or_adamw then the oracle round."""
+    segs = synth.fragment_segments(2048, [0, 8, 16], False)
+    n = synth.segments_numel(segs)
+    assert n == 151007616
+    M, p, r, B = 2, 0, 1, 0
+    cfg = cfg_for(B, tau=1)
+    rep = EmulatedReplicas(cfg, M, n)
+    A_d = synth.dev_init(torch.empty(n, device=DEV), segs, p)
+    Acopies = [A_d] + [A_d.clone() for _ in range(M - 1)]
+    v_d = [torch.zeros(n, device=DEV) for _ in range(M)]
+    th_d = []
+    for m in range(M):
+        th = A_d.clone()
+        synth.dev_apply_window(th, segs, p, m, r)
+        th_d.append(th)
+    A0 = synth.host_init(segs, p)
+    sends = [synth.host_apply_window(A0.copy(), segs, p, m, r) for m in range(M)]
+    if adamw:
+        hp = sd.SdAdamW(**HP)
+        rng = np.random.default_rng(5)
+        g = [(rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3)).astype(np.float32) for _ in range(M)]
+        m1 = [np.zeros(n, np.float32) for _ in range(M)]
+        m2 = [np.zeros(n, np.float32) for _ in range(M)]
+        m1_d, m2_d = [to_dev(x) for x in m1], [to_dev(x) for x in m2]
+        for m in range(M):
+            rep.ctx[m].sd_inner_adamw_quantize(p, 10, 1, th_d[m], to_dev(g[m]), m1_d[m], m2_d[m], Acopies[m],
+                                               rep.slot(m), hp, n)
+        for m in range(M):
+            rep.ctx[m].sd_fragment_sync(p, 10, rep.gather, n)
+        for m in range(M):
+            oracle.adamw(sends[m], g[m], m1[m], m2[m], 1, lr=HP["lr"], b1=HP["beta1"], b2=HP["beta2"], eps=HP["eps"],
+                         wd=HP["weight_decay"])
+    else:
+        rep.quantize_all(p, 10, th_d, Acopies)
+    for m in range(M):
+        synth.dev_apply_drift(th_d[m], segs, p, m, r)
+    rep.merge_all(p, 11, th_d, Acopies, v_d)
+    torch.cuda.synchronize()
+    merges = [synth.host_apply_drift(s.copy(), segs, p, m, r) for m, s in enumerate(sends)]
+    Ao, vo = A0.copy(), np.zeros(n, np.float32)
+    prev = oracle.threads()
+    oracle.set_threads(max(1, os.cpu_count() or 1))
+    try:
+        st, g_o = oracle.round_(sends, merges, Ao, vo, B=B)
+    finally:
+        oracle.set_threads(prev)
+    assert st == 0
+    got = rep.gather.cpu().numpy()
+    diff = np.nonzero(got != g_o)[0]
+    assert diff.size == 0, f"{diff.size} payload bytes differ, first at {diff[:8]}"
+    for m in range(M):
+        assert_same(Acopies[m], Ao, f"anchor {m}")
+        assert_same(v_d[m], vo, f"momentum {m}")
+        assert_same(th_d[m], merges[m], f"theta {m}")
     rep.close()
 
 
