@@ -40,7 +40,14 @@
  *  - Environment (read once per process): SD_BLOCKS_PER_SM=k caps the grids
  *    at k CTAs per SM (measurement switch, results bit-identical);
  *    SD_WAIT_TIMEOUT_MS bounds the fused gathers' block-receive (below);
- *    SD_LOG_INIT=1 prints one line per communicator set up (stderr).
+ *    SD_LOG_INIT=1 prints one line per communicator set up (stderr);
+ *    measurement switches of the staged two-pass quantize (results
+ *    bit-identical): SD_STAGE_HINTS (bit 0: pass 1 reads evict-first, bit 1:
+ *    pass 2 discards consumed summaries; default 3), SD_STAGE_L2_MB (MB of
+ *    summaries kept in L2 between the passes, default 40); SD_SIGNAL_KERNEL=0|1
+ *    forces the fused gathers' round signal into the payload kernel's last
+ *    CTA or a one-thread kernel after it (default: the kernel for push, the
+ *    last CTA for pull).
  */
 #ifndef SD_H_
 #define SD_H_
