@@ -41,6 +41,23 @@ MUTANTS = {
     "nibble_order": ("payload[k] = (uint8_t)(c0 | (c1 << 4));", "payload[k] = (uint8_t)(c1 | (c0 << 4));"),
     # or_e3m0_decode: wrong table index
     "decode_index": ("return LUT[code & 15] * s;", "return LUT[code & 7] * s;"),
+    # encoder: thresholds at the grid points instead of the log2 midpoints
+    "threshold_exponent": ("if (d2 >= ldexp(s2, -2 * j - 1)) ++e;", "if (d2 >= ldexp(s2, -2 * j)) ++e;"),
+    # encoder: code 8 (sign with e = 0) emitted for small negative values
+    "sign_on_zero_code": ("  if (e == 0) return 0; /* encoders emit s=0 with e=0 (S:264) */\n", ""),
+    # block scale: the first element instead of the max
+    "scale_first_element": ("    if (a > s) s = a;", "    if (i == 0) s = a;"),
+    # calendar: offsets rounded up instead of floor(p H / P)
+    "offset_rounding": ("return (int32_t)(((int64_t)p * c->H) / P);", "return (int32_t)(((int64_t)p * c->H + P - 1) / P);"),
+    # calendar: receive one step after send + tau
+    "receive_one_late": ("if (pending[p] + c->tau == t || t == c->T) {", "if (pending[p] + c->tau + 1 == t || t == c->T) {"),
+    # calendar: no flush of in-flight fragments at T
+    "no_flush": ("if (pending[p] + c->tau == t || t == c->T) {", "if (pending[p] + c->tau == t) {"),
+    # calendar: first send before a full window (t >= H dropped)
+    "first_send_before_H": ("if (t >= c->H && (t - tp) % c->H == 0) {", "if ((t - tp) % c->H == 0) {"),
+    # partition: sequential and strided patterns swapped
+    "pattern_swapped": ("out[k] = c->pattern == 0 ? p * c->fs + k : p + k * Pb;",
+                        "out[k] = c->pattern != 0 ? p * c->fs + k : p + k * Pb;"),
 }
 
 
@@ -70,12 +87,13 @@ def _caught(so):
     """Runs the pins against the library at `so`; returns the first failing pin or None."""
     import test_oracle_codec
     import test_oracle_outer
+    import test_oracle_schedule
 
     saved = dict(oracle._libs)
     oracle._libs["liboracle.so"] = oracle._load_path(so)
     prev = oracle.set_threads(1)
     try:
-        for mod in (test_oracle_outer, test_oracle_codec):
+        for mod in (test_oracle_outer, test_oracle_codec, test_oracle_schedule):
             for name, fn, kw in _pin_calls(mod):
                 try:
                     fn(**kw)

@@ -53,6 +53,14 @@ def test_offsets_examples():
         assert [oracle.offset(c, p) for p in range(len(case["offsets"]))] == case["offsets"]
 
 
+def test_offsets_at_the_baseline_configs():
+    """S:61 floor(p H / P) where the division is not exact (35M, 1B, 4B: SURVEY §8(a) a1)."""
+    for case in GOLD["offsets_configs"]["cases"]:
+        c = oracle.config(L=case["L"], fs=case["fs"], H=case["H"])
+        assert oracle.num_fragments(c) == len(case["offsets"]), case["name"]
+        assert [oracle.offset(c, p) for p in range(len(case["offsets"]))] == case["offsets"], case["name"]
+
+
 def test_fragment_counts_and_peak_reduction():
     # "8x" peak reduction = L/|p| fragments (P:276, P:501; AMB-19)
     for case in GOLD["fragment_counts"]["cases"]:
