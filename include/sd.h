@@ -347,7 +347,10 @@ sd_status sd_check(sd_ctx* ctx, int64_t* first_bad_index);
 /* Message of the last failing call on ctx (thread-local one if ctx == NULL). */
 const char* sd_last_error(const sd_ctx* ctx);
 
-/* Destroys the communicator, streams and events.  NULL is a no-op. */
+/* Destroys the communicator, streams and events and frees the gather buffers
+ * of sd_gather_alloc; with gather buffers or a workspace attached it first
+ * synchronizes the device, so the caller may free the workspace afterwards.
+ * NULL is a no-op. */
 sd_status sd_finalize(sd_ctx* ctx);
 
 /* Number of kernels libsd has launched in this process (for bench.py's

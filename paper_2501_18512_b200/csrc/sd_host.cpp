@@ -997,7 +997,7 @@ const char* sd_last_error(const sd_ctx* c) { return c ? c->err : g_err; }
 sd_status sd_finalize(sd_ctx* c) {
   if (!c) return SD_OK;
   cudaSetDevice(c->device);
-  if (!c->bufs.empty()) cudaDeviceSynchronize();
+  if (!c->bufs.empty() || c->ws.ptr) cudaDeviceSynchronize();  // before the caller may free the workspace
   for (GatherBuf& b : c->bufs) release(c, b);
   c->bufs.clear();
   if (c->comm) {

@@ -87,4 +87,5 @@ class FragmentSync:
 
     def close(self):
         self.gather = []
-        self.ctx.sd_finalize()
+        self.ctx.sd_finalize()  # synchronizes the device: the workspace is no longer in use
+        self.workspace = None
